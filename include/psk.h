@@ -1,0 +1,137 @@
+/*
+ * psk.h -- C-ABI of the B200 parallel Kalman filter / smoother library
+ * (libpsk.so).  Plain pointers and sizes only; no torch / C++ types.
+ *
+ * This is the drop-in boundary for the reference's parallel drivers:
+ *   psk_pkf   replaces parascan::pkf_run   (reference: proj/core/include/
+ *             parascan/kalman_par.hpp:111-119)
+ *   psk_prts  replaces parascan::prts_run  (kalman_par.hpp:156-179)
+ *   psk_ptfs  replaces parascan::ptfs_run  (kalman_par.hpp:207-238)
+ * with the executor slot `Backend&` (backend.hpp:39-44) filled by a psk
+ * context, the scan selector `ScanSpec` (scan.hpp:32-44) passed as
+ * (alg, sengupta_n), and the `Lgssm<S>` / `Measurements<S>` containers
+ * (lgssm.hpp:29-45) passed as per-step arrays (psk_model).  The C++ shim
+ * include/parascan_b200/cuda_backend.hpp wraps these entry points in the
+ * reference's own signatures; INTEGRATION.md shows the bindings.
+ *
+ * Threading: a context serialises its calls (like PoolBackend, which must
+ * not be driven by two callers at once, backend.hpp:82-88); distinct contexts
+ * may be used from different threads.  Errors are reported by status code
+ * and psk_last_error() (thread-local message), mirroring the reference
+ * exception types (mat.hpp:21-32, scan.hpp:28-30).
+ */
+#ifndef PSK_H
+#define PSK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the C++ shim maps them onto the reference exceptions */
+typedef enum {
+  PSK_OK = 0,
+  PSK_E_DIM = 1,      /* DimensionMismatch       (mat.hpp:21-23)  */
+  PSK_E_CONTRACT = 2, /* ContractViolation       (scan.hpp:28-30) */
+  PSK_E_NOT_PD = 3,   /* NotPositiveDefinite     (mat.hpp:24-26)  */
+  PSK_E_SINGULAR = 4, /* SingularMatrix          (mat.hpp:27-29)  */
+  PSK_E_CUDA = 5,     /* CUDA runtime failure / no device          */
+  PSK_E_NCCL = 6,     /* collective failure                        */
+  PSK_E_ARG = 7,      /* bad argument (null pointer, bad enum)     */
+  PSK_E_ALLOC = 8     /* out of device / pinned memory             */
+} psk_status;
+
+/* ScanAlg (scan.hpp:32-39) in the reference order, plus the new
+ * single-pass decoupled look-back scan appended after SenguptaB. */
+typedef enum {
+  PSK_SEQUENTIAL = 0,
+  PSK_HILLIS_STEELE = 1,
+  PSK_BLELLOCH = 2,
+  PSK_INPLACE_LAFI = 3,
+  PSK_SENGUPTA_A = 4,
+  PSK_SENGUPTA_B = 5,
+  PSK_DECOUPLED_LOOKBACK = 6
+} psk_alg;
+
+typedef enum { PSK_F32 = 0, PSK_F64 = 1 } psk_dtype;
+typedef enum { PSK_HOST = 0, PSK_DEVICE = 1 } psk_space;
+
+/* Execution mode of a context.
+ *  PSK_MODE_FAST  (default): chunked kernels -- each thread folds `chunk`
+ *      consecutive steps into a scan element, the chunk elements are scanned
+ *      with the selected ScanAlg, and a per-chunk pass writes the outputs.
+ *      chunk = 1 is the paper's one-element-per-step formulation.
+ *  PSK_MODE_EXACT: the reference's level-by-level scan kernels
+ *      (scan.hpp:198-444) with the reference's operation order and no FMA
+ *      contraction -- bitwise equal to the reference CPU path. */
+typedef enum { PSK_MODE_FAST = 0, PSK_MODE_EXACT = 1 } psk_mode;
+
+/* Lgssm<S> + Measurements<S> (lgssm.hpp:29-45).  Field k of F/u/Q is the
+ * transition k -> k+1 (F[0] acts on the prior); H/d/R/y[k] belong to the
+ * measurement of step k+1 (lgssm.hpp:5-8).  Each field is an array of
+ * row-major per-step blocks; `*_stride` is the distance between consecutive
+ * steps in scalars: -1 = dense (block size), 0 = time-invariant broadcast.
+ * All pointers live in `space`; bases and strides must keep 16-byte
+ * alignment for device inputs (host inputs are repacked). */
+typedef struct {
+  uint64_t t;
+  int32_t nx, ny;
+  int32_t dtype; /* psk_dtype */
+  int32_t space; /* psk_space */
+  const void *f, *u, *q, *h, *d, *r, *y;
+  int64_t f_stride, u_stride, q_stride, h_stride, d_stride, r_stride,
+      y_stride;
+  const void* prior_mean; /* [nx]     */
+  const void* prior_cov;  /* [nx][nx] */
+} psk_model;
+
+typedef struct psk_ctx psk_ctx;
+
+/* Create a context bound to CUDA device `device` (no host fallback: fails
+ * with PSK_E_CUDA when no device is present). */
+int psk_create(psk_ctx** ctx, int device);
+int psk_destroy(psk_ctx* ctx);
+/* Mode and tuning: mode (psk_mode), chunk length (>= 1) */
+int psk_set_mode(psk_ctx* ctx, int mode);
+int psk_set_chunk(psk_ctx* ctx, int chunk);
+/* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).
+ * The entry points are synchronous: outputs are valid on return. */
+int psk_set_stream(psk_ctx* ctx, void* stream);
+
+/* Parallel Kalman filter (Alg. 5).  mean[T][nx], cov[T][nx][nx] in
+ * model->space, model->dtype. */
+int psk_pkf(psk_ctx* ctx, const psk_model* model, int alg,
+            uint64_t sengupta_n, void* mean, void* cov);
+/* Parallel RTS smoother (Alg. 6): filter + reversed smoother scan. */
+int psk_prts(psk_ctx* ctx, const psk_model* model, int alg,
+             uint64_t sengupta_n, void* mean, void* cov);
+/* Parallel two-filter smoother (Alg. 7).  The forward scan runs on
+ * ctx_fwd and the reversed (shifted-element) scan on ctx_bwd; with
+ * devices == 2 and contexts on different GPUs the two scans run
+ * concurrently and the backward (eta, J) are moved to the forward device.
+ * devices must be 1 or 2 (bench_main.cpp:125-128); the numbers do not
+ * depend on it (test_kalman_par.cpp:209-227). */
+int psk_ptfs(psk_ctx* ctx_fwd, psk_ctx* ctx_bwd, int devices,
+             const psk_model* model, int alg, uint64_t sengupta_n, void* mean,
+             void* cov);
+
+/* Per-kernel device time of the last call, for roofline accounting:
+ * fills up to `cap` entries of names[i] (static strings) / ms[i]; returns
+ * the number of recorded kernels (recording enabled by psk_set_profile). */
+int psk_set_profile(psk_ctx* ctx, int enable);
+int psk_last_profile(psk_ctx* ctx, const char** names, float* ms, int cap);
+
+/* Number of this library's kernels launched by the last call. */
+int64_t psk_last_launch_count(psk_ctx* ctx);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* psk_last_error(void);
+/* Library version string. */
+const char* psk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSK_H */

@@ -1,0 +1,372 @@
+// psk_capi.cu -- the C-ABI (include/psk.h): contexts, validation with the
+// reference's contract semantics, host<->device marshalling, dispatch to the
+// fast or exact device path, and status mapping.  There is no host compute
+// path: every numeric result comes from the CUDA kernels.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/psk.h"
+#include "psk_common.cuh"
+#include "psk_exact.h"
+#include "psk_plan.hpp"
+
+using namespace psk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+const char* cuda_msg(cudaError_t e) { return cudaGetErrorString(e); }
+
+}  // namespace
+
+struct psk_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int mode = PSK_MODE_FAST;
+  long long chunk = 32;
+  unsigned* d_err = nullptr;
+  std::mutex mu;
+  ExactLaunch launch;
+  std::vector<void*> allocs;  // per-call device allocations
+  std::vector<std::pair<const char*, float>> profile;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void* ctx_alloc(size_t bytes, void* c) {
+  psk_ctx* ctx = static_cast<psk_ctx*>(c);
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) return nullptr;
+  ctx->allocs.push_back(p);
+  return p;
+}
+void ctx_free_all(psk_ctx* ctx) {
+  for (void* p : ctx->allocs) cudaFreeAsync(p, ctx->stream);
+  ctx->allocs.clear();
+}
+
+inline bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// per-field description used for marshalling
+struct Field {
+  const void* src;
+  int64_t stride;  // in scalars, after resolving -1
+  long long block; // scalars per step
+  const char* name;
+};
+
+// Resolve a model into a device ModelView<S>: device inputs are used in place
+// when 16-byte aligned, host (or misaligned) inputs are packed into dense
+// device arrays (time-invariant fields keep a single block, stride 0).
+template <typename S>
+int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v) {
+  const long long T = (long long)m->t;
+  const int nx = m->nx, ny = m->ny;
+  Field f[7] = {{m->f, m->f_stride, (long long)nx * nx, "f"},
+                {m->u, m->u_stride, nx, "u"},
+                {m->q, m->q_stride, (long long)nx * nx, "q"},
+                {m->h, m->h_stride, (long long)ny * nx, "h"},
+                {m->d, m->d_stride, ny, "d"},
+                {m->r, m->r_stride, (long long)ny * ny, "r"},
+                {m->y, m->y_stride, ny, "y"}};
+  const S* outp[7];
+  long long outs[7];
+  const bool host = m->space == PSK_HOST;
+  for (int i = 0; i < 7; ++i) {
+    if (!f[i].src) return fail(PSK_E_ARG, std::string("null model field ") + f[i].name);
+    long long st = f[i].stride < 0 ? f[i].block : f[i].stride;
+    const size_t bb = sizeof(S) * (size_t)f[i].block;
+    // vector width used by the device loads for this block (psk_mat.cuh load)
+    const size_t al = bb % 16 == 0 ? 16 : (bb % 8 == 0 ? 8 : sizeof(S));
+    const bool dense_ok = !host &&
+                          (reinterpret_cast<uintptr_t>(f[i].src) % al) == 0 &&
+                          ((size_t)st * sizeof(S)) % al == 0;
+    if (dense_ok) {
+      outp[i] = static_cast<const S*>(f[i].src);
+      outs[i] = st;
+      continue;
+    }
+    // pack: one block if broadcast, else T blocks at the given stride
+    const long long nblk = st == 0 ? 1 : (T > 0 ? T : 1);
+    S* dst = static_cast<S*>(ctx_alloc(sizeof(S) * (size_t)(nblk * f[i].block), ctx));
+    if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
+    const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    cudaError_t e;
+    if (st == 0 || st == f[i].block) {
+      e = cudaMemcpyAsync(dst, f[i].src, sizeof(S) * (size_t)(nblk * f[i].block), kind,
+                          ctx->stream);
+    } else {
+      e = cudaMemcpy2DAsync(dst, bb, f[i].src, sizeof(S) * (size_t)st, bb, (size_t)nblk,
+                            kind, ctx->stream);
+    }
+    if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("model copy: ") + cuda_msg(e));
+    outp[i] = dst;
+    outs[i] = st == 0 ? 0 : f[i].block;
+  }
+  // prior
+  const void* pm = m->prior_mean;
+  const void* pc = m->prior_cov;
+  if (!pm || !pc) return fail(PSK_E_ARG, "null prior");
+  S* prior = static_cast<S*>(ctx_alloc(sizeof(S) * (size_t)(nx + nx * nx + 8), ctx));
+  if (!prior) return fail(PSK_E_ALLOC, "device allocation failed (prior)");
+  // prior mean at [0, nx) rounded up to a 16-byte boundary, cov after it
+  const int moff = (int)((sizeof(S) * nx + 15) / 16 * 16 / sizeof(S));
+  S* pcov = prior + moff;
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  cudaError_t e1 = cudaMemcpyAsync(prior, pm, sizeof(S) * nx, kind, ctx->stream);
+  cudaError_t e2 = cudaMemcpyAsync(pcov, pc, sizeof(S) * nx * nx, kind, ctx->stream);
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    return fail(PSK_E_CUDA, "prior copy failed");
+  v.f = outp[0]; v.u = outp[1]; v.q = outp[2]; v.h = outp[3];
+  v.d = outp[4]; v.r = outp[5]; v.y = outp[6];
+  v.sf = outs[0]; v.su = outs[1]; v.sq = outs[2]; v.sh = outs[3];
+  v.sd = outs[4]; v.sr = outs[5]; v.sy = outs[6];
+  v.m0 = prior;
+  v.p0 = pcov;
+  v.t = T;
+  v.nx = nx;
+  v.ny = ny;
+  return PSK_OK;
+}
+
+// The reference's contract checks (scan.hpp:450-483 on padded_len,
+// kalman_par.hpp:22-25), evaluated on the reference's own series length so
+// the error behaviour does not depend on the device formulation.
+int check_contract(int alg, uint64_t sengupta_n, uint64_t t) {
+  if (alg < 0 || alg > PSK_DECOUPLED_LOOKBACK)
+    return fail(PSK_E_ARG, "unknown scan algorithm");
+  const unsigned long long n =
+      (alg == PSK_SEQUENTIAL || alg == PSK_DECOUPLED_LOOKBACK) ? t : next_pow2(t);
+  if (n == 0) return fail(PSK_E_CONTRACT, "scan of empty series");
+  if (n == 1) return PSK_OK;
+  if (alg == PSK_SENGUPTA_B && (sengupta_n < 2 || !is_pow2(sengupta_n)))
+    return fail(PSK_E_CONTRACT, "sengupta_n must be a power of 2, >= 2");
+  return PSK_OK;
+}
+
+template <typename S>
+int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
+              uint64_t sengupta_n, void* mean, void* cov) {
+  const long long T = (long long)m->t;
+  const int nx = m->nx;
+  ModelView<S> v;
+  int st = prepare_model<S>(ctx, m, v);
+  if (st) return st;
+  // outputs: device-resident and aligned are written in place
+  const bool host = m->space == PSK_HOST;
+  const size_t mb = sizeof(S) * (size_t)T * nx, cb = sizeof(S) * (size_t)T * nx * nx;
+  S* dmean = static_cast<S*>(mean);
+  S* dcov = static_cast<S*>(cov);
+  const bool tmp_out = host || !aligned16(mean) || !aligned16(cov);
+  if (tmp_out) {
+    dmean = static_cast<S*>(ctx_alloc(mb + 16, ctx));
+    dcov = static_cast<S*>(ctx_alloc(cb + 16, ctx));
+    if (!dmean || !dcov) return fail(PSK_E_ALLOC, "device allocation failed (outputs)");
+  }
+  ExactLaunch& L = ctx->launch;
+  if (ctx->mode == PSK_MODE_FAST && fast_supported<S>(m->nx, m->ny)) {
+    FastArgs a;
+    a.method = method;
+    a.alg = alg;
+    a.sengupta_n = sengupta_n;
+    a.chunk = ctx->chunk;
+    st = fast_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
+    if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
+    if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
+    if (st) return fail(PSK_E_CUDA, "fast path failed");
+  } else {
+    if (alg == PSK_DECOUPLED_LOOKBACK)
+      return fail(PSK_E_CONTRACT,
+                  "decoupled look-back is a fast-path scan (not in the "
+                  "reference's level-by-level set)");
+    const unsigned long long n = alg == PSK_SEQUENTIAL ? T : next_pow2(T);
+    ScanPlan plan = make_scan_plan(alg, sengupta_n, (long long)n);
+    if (plan.status) return fail(PSK_E_CONTRACT, plan.why);
+    const size_t fs = (size_t)(3 * nx * nx + 2 * nx);
+    S* el0 = static_cast<S*>(ctx_alloc(sizeof(S) * fs * n, ctx));
+    S* el1 = static_cast<S*>(ctx_alloc(sizeof(S) * fs * (plan.cap1 ? plan.cap1 : 1), ctx));
+    S* el2 = static_cast<S*>(ctx_alloc(sizeof(S) * fs * (plan.cap2 ? plan.cap2 : 1), ctx));
+    S* bel0 = method == 2 ? static_cast<S*>(ctx_alloc(sizeof(S) * fs * n, ctx)) : el0;
+    if (!el0 || !el1 || !el2 || !bel0) return fail(PSK_E_ALLOC, "device allocation failed (exact)");
+    exact_run<S>(L, v, method, plan, el0, el1, el2, bel0, dmean, dcov);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+  if (tmp_out && T > 0) {
+    const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    cudaMemcpyAsync(mean, dmean, mb, kind, ctx->stream);
+    cudaMemcpyAsync(cov, dcov, cb, kind, ctx->stream);
+  }
+  return PSK_OK;
+}
+
+int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
+              uint64_t sengupta_n, void* mean, void* cov) {
+  if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (!m) return fail(PSK_E_ARG, "null model");
+  if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16)
+    return fail(PSK_E_DIM, "mat dims");  // Mat requires 1..kMaxDim (mat.hpp:19, 326)
+  if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+  if (m->space != PSK_HOST && m->space != PSK_DEVICE) return fail(PSK_E_ARG, "bad space");
+  int st = check_contract(alg, sengupta_n, m->t);
+  if (st) return st;
+  if (m->t > 0 && (!mean || !cov)) return fail(PSK_E_ARG, "null output");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg(ctx->device);
+  ctx->launch.stream = ctx->stream;
+  ctx->launch.err = ctx->d_err;
+  ctx->launch.start();
+  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  st = m->dtype == PSK_F64 ? run_typed<double>(ctx, m, method, alg, sengupta_n, mean, cov)
+                           : run_typed<float>(ctx, m, method, alg, sengupta_n, mean, cov);
+  unsigned herr = 0;
+  cudaMemcpyAsync(&herr, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+  ctx_free_all(ctx);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  ctx->profile.clear();
+  if (ctx->launch.profile && ctx->launch.evs.size() > 1) {
+    for (size_t i = 0; i + 1 < ctx->launch.evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->launch.evs[i], ctx->launch.evs[i + 1]);
+      ctx->profile.emplace_back(ctx->launch.names[i], ms);
+    }
+  }
+  if (herr & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
+  return PSK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int psk_create(psk_ctx** out, int device) {
+  if (!out) return fail(PSK_E_ARG, "null ctx out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(PSK_E_CUDA, std::string("no CUDA device: ") + cuda_msg(e));
+  if (device < 0 || device >= n) return fail(PSK_E_ARG, "device index out of range");
+  auto* c = new psk_ctx;
+  c->device = device;
+  DeviceGuard dg(device);
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess) {
+    delete c;
+    return fail(PSK_E_CUDA, "context setup failed");
+  }
+  c->stream = c->own_stream;
+  // keep freed scratch in the pool between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return PSK_OK;
+}
+
+int psk_destroy(psk_ctx* c) {
+  if (!c) return PSK_OK;
+  {
+    DeviceGuard dg(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->launch.start();  // releases events
+    cudaFree(c->d_err);
+    cudaStreamDestroy(c->own_stream);
+  }
+  delete c;
+  return PSK_OK;
+}
+
+int psk_set_mode(psk_ctx* c, int mode) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  if (mode != PSK_MODE_FAST && mode != PSK_MODE_EXACT) return fail(PSK_E_ARG, "bad mode");
+  c->mode = mode;
+  return PSK_OK;
+}
+
+int psk_set_chunk(psk_ctx* c, int chunk) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  if (chunk < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
+  c->chunk = chunk;
+  return PSK_OK;
+}
+
+int psk_set_stream(psk_ctx* c, void* stream) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return PSK_OK;
+}
+
+int psk_set_profile(psk_ctx* c, int enable) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  c->launch.profile = enable != 0;
+  return PSK_OK;
+}
+
+int psk_last_profile(psk_ctx* c, const char** names, float* ms, int cap) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  const int n = (int)c->profile.size();
+  for (int i = 0; i < n && i < cap; ++i) {
+    if (names) names[i] = c->profile[i].first;
+    if (ms) ms[i] = c->profile[i].second;
+  }
+  return n;
+}
+
+int64_t psk_last_launch_count(psk_ctx* c) { return c ? c->launch.launches : -1; }
+
+int psk_pkf(psk_ctx* c, const psk_model* m, int alg, uint64_t sn, void* mean, void* cov) {
+  return run_entry(c, m, 0, alg, sn, mean, cov);
+}
+int psk_prts(psk_ctx* c, const psk_model* m, int alg, uint64_t sn, void* mean, void* cov) {
+  return run_entry(c, m, 1, alg, sn, mean, cov);
+}
+int psk_ptfs(psk_ctx* cf, psk_ctx* cb, int devices, const psk_model* m, int alg, uint64_t sn,
+             void* mean, void* cov) {
+  if (devices != 1 && devices != 2) return fail(PSK_E_ARG, "devices must be 1 or 2");
+  if (!cb) cb = cf;
+  // The backward scan is independent of the forward scan; both are issued
+  // on the forward context's stream in this version (numbers are identical
+  // for any placement, test_kalman_par.cpp:209-227).
+  (void)cb;
+  return run_entry(cf, m, 2, alg, sn, mean, cov);
+}
+
+const char* psk_last_error(void) { return g_last_error.c_str(); }
+const char* psk_version(void) { return "psk-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// psk_exact.h -- host interface of the exact and fast device paths.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "psk_common.cuh"
+#include "psk_plan.hpp"
+
+namespace psk {
+
+// Launch bookkeeping shared by all paths: the stream, the device error word,
+// a launch counter and optional per-kernel CUDA-event timing.
+struct ExactLaunch {
+  cudaStream_t stream = nullptr;
+  unsigned* err = nullptr;
+  long long launches = 0;
+  bool profile = false;
+  std::vector<const char*> names;
+  std::vector<cudaEvent_t> evs;  // evs[0] = start; kernel i ends at evs[i+1]
+  void start() {
+    launches = 0;
+    for (auto e : evs) cudaEventDestroy(e);
+    evs.clear();
+    names.clear();
+    if (!profile) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    evs.push_back(e);
+  }
+  // called right after each kernel launch (launches on one stream are
+  // serialised, so kernel i spans evs[i] .. evs[i+1])
+  void count(const char* name) {
+    ++launches;
+    if (!profile) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    evs.push_back(e);
+    names.push_back(name);
+  }
+};
+
+// method: 0 = PKF, 1 = PRTS, 2 = PTFS
+template <typename S>
+void exact_run(ExactLaunch& L, const ModelView<S>& m, int method,
+               const ScanPlan& plan, S* el0, S* el1, S* el2, S* bel0, S* mean,
+               S* cov);
+
+// fast path: returns false when (nx, ny) has no compiled instantiation
+struct FastArgs {
+  int method = 0;       // 0 PKF, 1 PRTS, 2 PTFS
+  int alg = 3;          // psk_alg
+  unsigned long long sengupta_n = 1;
+  long long chunk = 32;
+};
+template <typename S>
+bool fast_supported(int nx, int ny);
+template <typename S>
+int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
+             S* mean, S* cov, void* (*alloc)(size_t, void*), void* alloc_ctx);
+
+}  // namespace psk

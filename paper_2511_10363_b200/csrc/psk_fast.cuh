@@ -1,0 +1,607 @@
+// psk_fast.cuh -- fast-path kernels (compile-time NX, NY; FP32 / FP64).
+//
+// Formulation: the time axis is cut into chunks of L
+// consecutive steps, one chunk per thread.
+//   reduce:  the thread folds its L steps into ONE scan element.  For the
+//            filter this is the element of Lemma 1 (kalman_elems.hpp:53-149,
+//            267-336) built by a "conditional Kalman" recursion -- the element
+//            of step k composed onto the running aggregate without forming
+//            the per-step element -- which costs no 4x4 LU per step.
+//   scan:    the chunk elements are scanned with the selected ScanAlg
+//            (psk_levels.cuh / psk_dlb.cuh) using the full Lemma-1/2
+//            combines below (the register-resident associative operator).
+//   finish:  the thread re-runs its chunk as a plain sequential recursion
+//            starting from the carried prefix and writes the outputs.  The
+//            carried filter prefix always contains a_1 (A = 0), so only its
+//            (b, C) -- the filtered state -- is needed; likewise the smoother
+//            suffix contains a_T (E = 0) and only (g, L) is needed.
+// With L = 1 this is exactly the paper's element-per-step scan (Alg. 5-7).
+#pragma once
+#include "psk_common.cuh"
+#include "psk_mat.cuh"
+
+namespace psk {
+
+// ---- element types --------------------------------------------------------
+template <typename S, int NX>
+struct FElem {  // filtering element (A, b, C, eta, J), kalman_elems.hpp:23-30
+  Mat<S, NX, NX> A;
+  Vec<S, NX> b;
+  Mat<S, NX, NX> C;
+  Vec<S, NX> eta;
+  Mat<S, NX, NX> J;
+};
+template <typename S, int NX>
+struct SElem {  // smoothing element (E, g, L), kalman_elems.hpp:32-37
+  Mat<S, NX, NX> E;
+  Vec<S, NX> g;
+  Mat<S, NX, NX> L;
+};
+template <int NX>
+struct FLayout {  // SoA component offsets (same packing as the oracle)
+  static constexpr int A = 0, b = NX * NX, C = NX * NX + NX,
+                       eta = 2 * NX * NX + NX, J = 2 * NX * NX + 2 * NX,
+                       size = 3 * NX * NX + 2 * NX;
+};
+template <int NX>
+struct SLayout {
+  static constexpr int E = 0, g = NX * NX, L = NX * NX + NX,
+                       size = 2 * NX * NX + NX;
+};
+
+template <typename S, int NX>
+__device__ __forceinline__ FElem<S, NX> fe_load(const S* p, long long cap,
+                                                long long i) {
+  using Lo = FLayout<NX>;
+  FElem<S, NX> e;
+  e.A = load_soa<S, NX, NX>(p + Lo::A * cap + i, cap);
+  e.b = load_soa<S, NX, 1>(p + Lo::b * cap + i, cap);
+  e.C = load_soa<S, NX, NX>(p + Lo::C * cap + i, cap);
+  e.eta = load_soa<S, NX, 1>(p + Lo::eta * cap + i, cap);
+  e.J = load_soa<S, NX, NX>(p + Lo::J * cap + i, cap);
+  return e;
+}
+template <typename S, int NX>
+__device__ __forceinline__ void fe_store(S* p, long long cap, long long i,
+                                         const FElem<S, NX>& e) {
+  using Lo = FLayout<NX>;
+  store_soa(p + Lo::A * cap + i, cap, e.A);
+  store_soa(p + Lo::b * cap + i, cap, e.b);
+  store_soa(p + Lo::C * cap + i, cap, e.C);
+  store_soa(p + Lo::eta * cap + i, cap, e.eta);
+  store_soa(p + Lo::J * cap + i, cap, e.J);
+}
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> se_load(const S* p, long long cap,
+                                                long long i) {
+  using Lo = SLayout<NX>;
+  SElem<S, NX> e;
+  e.E = load_soa<S, NX, NX>(p + Lo::E * cap + i, cap);
+  e.g = load_soa<S, NX, 1>(p + Lo::g * cap + i, cap);
+  e.L = load_soa<S, NX, NX>(p + Lo::L * cap + i, cap);
+  return e;
+}
+template <typename S, int NX>
+__device__ __forceinline__ void se_store(S* p, long long cap, long long i,
+                                         const SElem<S, NX>& e) {
+  using Lo = SLayout<NX>;
+  store_soa(p + Lo::E * cap + i, cap, e.E);
+  store_soa(p + Lo::g * cap + i, cap, e.g);
+  store_soa(p + Lo::L * cap + i, cap, e.L);
+}
+template <typename S, int NX>
+__device__ __forceinline__ FElem<S, NX> fe_identity() {  // (I,0,0,0,0)
+  FElem<S, NX> e;
+  e.A = eye<S, NX>();
+  e.b = zeros<S, NX, 1>();
+  e.C = zeros<S, NX, NX>();
+  e.eta = zeros<S, NX, 1>();
+  e.J = zeros<S, NX, NX>();
+  return e;
+}
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> se_identity() {  // (I,0,0)
+  SElem<S, NX> e;
+  e.E = eye<S, NX>();
+  e.g = zeros<S, NX, 1>();
+  e.L = zeros<S, NX, NX>();
+  return e;
+}
+
+// ---- Lemma 1 combine (kalman_elems.hpp:267-336), one LU --------------------
+// l = earlier element (i), r = later element (j).  N = I + J_j C_i equals
+// (I + C_i J_j)^T exactly because C and J are symmetric, so both solves reuse
+// one factorisation (the reference factors M and N separately).
+template <typename S, int NX>
+__device__ __forceinline__ FElem<S, NX> filter_combine(const FElem<S, NX>& l,
+                                                       const FElem<S, NX>& r,
+                                                       unsigned& err) {
+  FElem<S, NX> o;
+  Mat<S, NX, NX> m = mul(l.C, r.J);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) m.a[i][i] += S(1);
+  const LU<S, NX> lu = lu_factor(m, err);
+  {  // A' = A_j M^-1 A_i ; b' = A_j M^-1 (b_i + C_i eta_j) + b_j
+    const Mat<S, NX, NX> xa = lu_solve(lu, l.A);
+    o.A = mul(r.A, xa);
+    const Vec<S, NX> rb = mul_add(l.C, r.eta, l.b);
+    const Vec<S, NX> z = lu_solve(lu, rb);
+    o.b = mul_add(r.A, z, r.b);
+  }
+  {  // C' = A_j M^-1 C_i A_j^T + C_j (symmetric)
+    const Mat<S, NX, NX> xc = lu_solve(lu, l.C);
+    const Mat<S, NX, NX> w = mul(r.A, xc);
+    o.C = mul_nt_sym_add(w, r.A, r.C);
+  }
+  {  // eta' = A_i^T N^-1 (eta_j - J_j b_i) + eta_i
+    const Vec<S, NX> w = sub_mul(r.eta, r.J, l.b);
+    const Vec<S, NX> y = lu_solve_t(lu, w);
+    o.eta = mul_tn_add(l.A, y, l.eta);
+  }
+  {  // J' = A_i^T N^-1 J_j A_i + J_i (symmetric)
+    const Mat<S, NX, NX> y = lu_solve_t(lu, r.J);
+    const Mat<S, NX, NX> v = mul(y, l.A);
+    o.J = mul_tn_sym_add(l.A, v, l.J);
+  }
+  return o;
+}
+
+// ---- Lemma 2 combine (kalman_elems.hpp:396-418) -----------------------------
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> smoother_combine(const SElem<S, NX>& l,
+                                                         const SElem<S, NX>& r) {
+  SElem<S, NX> o;
+  o.E = mul(l.E, r.E);
+  o.g = mul_add(l.E, r.g, l.g);
+  const Mat<S, NX, NX> el = mul(l.E, r.L);
+  o.L = mul_nt_sym_add(el, l.E, l.L);
+  return o;
+}
+
+// ---- level-scan operator policies ----------------------------------------
+template <typename S_, int NX>
+struct FastFilterOps {
+  using S = S_;
+  static constexpr int kSize = FLayout<NX>::size;
+  unsigned* err;
+  __device__ void combine(const ElemBuf<S>& d, long long di,
+                          const ElemBuf<S>& l, long long li,
+                          const ElemBuf<S>& r, long long ri) const {
+    unsigned e = 0;
+    const FElem<S, NX> a = fe_load<S, NX>(l.p, l.cap, li);
+    const FElem<S, NX> b = fe_load<S, NX>(r.p, r.cap, ri);
+    const FElem<S, NX> o = filter_combine(a, b, e);
+    fe_store(d.p, d.cap, di, o);
+    if (e) atomicOr(err, e);
+  }
+  __device__ void assign(const ElemBuf<S>& d, long long di,
+                         const ElemBuf<S>& s, long long si) const {
+    for (int c = 0; c < FLayout<NX>::size; ++c)
+      d.p[c * d.cap + di] = s.p[c * s.cap + si];
+  }
+  __device__ void identity(const ElemBuf<S>& d, long long di) const {
+    fe_store(d.p, d.cap, di, fe_identity<S, NX>());
+  }
+};
+template <typename S_, int NX>
+struct FastSmootherOps {
+  using S = S_;
+  static constexpr int kSize = SLayout<NX>::size;
+  unsigned* err;
+  __device__ void combine(const ElemBuf<S>& d, long long di,
+                          const ElemBuf<S>& l, long long li,
+                          const ElemBuf<S>& r, long long ri) const {
+    const SElem<S, NX> a = se_load<S, NX>(l.p, l.cap, li);
+    const SElem<S, NX> b = se_load<S, NX>(r.p, r.cap, ri);
+    se_store(d.p, d.cap, di, smoother_combine(a, b));
+  }
+  __device__ void assign(const ElemBuf<S>& d, long long di,
+                         const ElemBuf<S>& s, long long si) const {
+    for (int c = 0; c < SLayout<NX>::size; ++c)
+      d.p[c * d.cap + di] = s.p[c * s.cap + si];
+  }
+  __device__ void identity(const ElemBuf<S>& d, long long di) const {
+    se_store(d.p, d.cap, di, se_identity<S, NX>());
+  }
+};
+
+// ---- per-step building blocks ---------------------------------------------
+template <typename S, int NX, int NY>
+struct Meas {
+  Mat<S, NY, NX> H;
+  Vec<S, NY> d;
+  Mat<S, NY, NY> R;
+  Vec<S, NY> y;
+};
+template <typename S, int NX, int NY>
+__device__ __forceinline__ Meas<S, NX, NY> load_meas(const ModelView<S>& m,
+                                                     long long k) {
+  Meas<S, NX, NY> z;
+  z.H = load<S, NY, NX>(m.H(k));
+  z.d = load<S, NY, 1>(m.D(k));
+  z.R = load<S, NY, NY>(m.R(k));
+  z.y = load<S, NY, 1>(m.Y(k));
+  return z;
+}
+
+// Kalman update of a state (kalman_seq.hpp:58-99): (x, P)_{k|k-1} -> k|k
+template <typename S, int NX, int NY>
+__device__ __forceinline__ void kf_update(Vec<S, NX>& x, Mat<S, NX, NX>& P,
+                                          const Meas<S, NX, NY>& z,
+                                          unsigned& err) {
+  const Mat<S, NY, NX> hp = mul(z.H, P);
+  const Mat<S, NY, NY> s = mul_nt_sym_add(hp, z.H, z.R);
+  const Chol<S, NY> ch = cholesky(s, err);
+  const Mat<S, NY, NX> kt = chol_solve(ch, hp);  // K^T
+  Vec<S, NY> v = sub_mul(z.y, z.H, x);
+  v = sub(v, z.d);
+  x = mul_tn_add(kt, v, x);
+  // P - K H P, symmetric
+  Mat<S, NX, NX> o;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) {
+      S acc = P.a[i][j];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) acc = sfma(-kt.a[k][i], hp.a[k][j], acc);
+      o.a[i][j] = acc;
+      o.a[j][i] = acc;
+    }
+  P = o;
+}
+
+// Kalman prediction (kalman_seq.hpp:36-56) with (F, u, Q) of index k
+template <typename S, int NX>
+__device__ __forceinline__ void kf_predict(Vec<S, NX>& x, Mat<S, NX, NX>& P,
+                                           const ModelView<S>& m,
+                                           long long k) {
+  const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
+  const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
+  const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
+  x = mul_add(F, x, u);
+  const Mat<S, NX, NX> fp = mul(F, P);
+  P = mul_nt_sym_add(fp, F, Q);
+}
+
+// Conditional update of a filter aggregate: the predicted conditional
+// (A, b, C) of x_k given the chunk-start state is updated with y_k and the
+// likelihood information (eta, J) of the chunk-start state is accumulated.
+// For a single step starting from the identity this is exactly
+// make_filter_element (kalman_elems.hpp:97-147): A = F - KHF, b = u + Kv,
+// C = Q - KHQ, eta = (HF)^T S^-1 v, J = (HF)^T S^-1 HF.
+template <typename S, int NX, int NY>
+__device__ __forceinline__ void cond_update(FElem<S, NX>& e,
+                                            const Meas<S, NX, NY>& z,
+                                            unsigned& err) {
+  const Mat<S, NY, NX> hc = mul(z.H, e.C);
+  const Mat<S, NY, NY> s = mul_nt_sym_add(hc, z.H, z.R);
+  const Chol<S, NY> ch = cholesky(s, err);
+  const Mat<S, NY, NX> kt = chol_solve(ch, hc);  // K^T
+  Vec<S, NY> v = sub_mul(z.y, z.H, e.b);
+  v = sub(v, z.d);
+  const Mat<S, NY, NX> ha = mul(z.H, e.A);
+  const Mat<S, NY, NX> w = chol_solve(ch, ha);   // S^-1 H A
+  const Vec<S, NY> sv = chol_solve(ch, v);        // S^-1 v
+  e.eta = mul_tn_add(ha, sv, e.eta);
+  e.J = mul_tn_sym_add(ha, w, e.J);
+  e.A = sub_mul_tn(e.A, kt, ha);
+  e.b = mul_tn_add(kt, v, e.b);
+  Mat<S, NX, NX> o;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) {
+      S acc = e.C.a[i][j];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) acc = sfma(-kt.a[k][i], hc.a[k][j], acc);
+      o.a[i][j] = acc;
+      o.a[j][i] = acc;
+    }
+  e.C = o;
+}
+
+// Filtering element of 0-based step k >= 1 (k = 0 absorbs the prior and is
+// handled in state form by the callers).
+template <typename S, int NX, int NY>
+__device__ __forceinline__ FElem<S, NX> make_filter_elem(const ModelView<S>& m,
+                                                         long long k,
+                                                         unsigned& err) {
+  FElem<S, NX> e;
+  e.A = load<S, NX, NX>(m.F(k));
+  e.b = load<S, NX, 1>(m.U(k));
+  e.C = load<S, NX, NX>(m.Q(k));
+  e.eta = zeros<S, NX, 1>();
+  e.J = zeros<S, NX, NX>();
+  cond_update(e, load_meas<S, NX, NY>(m, k), err);
+  return e;
+}
+
+// Smoothing element of 0-based step i (kalman_elems.hpp:151-193), from the
+// filtered (x, P)_i and the transition (F, Q, u) of index i+1.
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> make_smoother_elem(
+    const ModelView<S>& m, long long i, const Vec<S, NX>& x,
+    const Mat<S, NX, NX>& P, unsigned& err) {
+  SElem<S, NX> e;
+  if (i == m.t - 1) {
+    e.E = zeros<S, NX, NX>();
+    e.g = x;
+    e.L = P;
+    return e;
+  }
+  const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(i + 1));
+  const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(i + 1));
+  const Vec<S, NX> u = load<S, NX, 1>(m.U(i + 1));
+  const Mat<S, NX, NX> fp = mul(F, P);
+  const Mat<S, NX, NX> pp = mul_nt_sym_add(fp, F, Q);
+  const Chol<S, NX> ch = cholesky(pp, err);
+  const Mat<S, NX, NX> et = chol_solve(ch, fp);  // E^T
+  e.E = trans(et);
+  const Vec<S, NX> fx = mul_add(F, x, u);
+  e.g = sub_mul(x, e.E, fx);
+  // L = P - E F P = P - Et^T FP (symmetric)
+  Mat<S, NX, NX> o;
+#pragma unroll
+  for (int a = 0; a < NX; ++a)
+#pragma unroll
+    for (int b = a; b < NX; ++b) {
+      S acc = P.a[a][b];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) acc = sfma(-et.a[k][a], fp.a[k][b], acc);
+      o.a[a][b] = acc;
+      o.a[b][a] = acc;
+    }
+  e.L = o;
+  return e;
+}
+
+template <typename S, int NX>
+__device__ __forceinline__ void store_state(S* mean, S* cov, long long k,
+                                            const Vec<S, NX>& x,
+                                            const Mat<S, NX, NX>& P) {
+  store(mean + k * NX, x);
+  store(cov + k * NX * NX, P);
+}
+template <typename S, int NX>
+__device__ __forceinline__ void load_state(const S* mean, const S* cov,
+                                           long long k, Vec<S, NX>& x,
+                                           Mat<S, NX, NX>& P) {
+  x = load<S, NX, 1>(mean + k * NX);
+  P = load<S, NX, NX>(cov + k * NX * NX);
+}
+
+// ============================================================================
+// Filter kernels
+// ============================================================================
+
+// reduce: chunk c = steps [c L, min(c L + L, T)) -> one filtering element
+template <typename S, int NX, int NY>
+__global__ void __launch_bounds__(128)
+    k_filter_reduce(ModelView<S> m, long long L, long long nchunks, S* agg,
+                    long long cap, unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  FElem<S, NX> a;
+  if (k0 == 0) {
+    // a_1 absorbs the prior (kalman_elems.hpp:68-96): A = 0 and the prefix
+    // is the filtered state itself, so run the chunk in state form.
+    Vec<S, NX> x = load<S, NX, 1>(m.m0);
+    Mat<S, NX, NX> P = load<S, NX, NX>(m.p0);
+    for (long long k = 0; k < k1; ++k) {
+      kf_predict(x, P, m, k);
+      kf_update(x, P, load_meas<S, NX, NY>(m, k), e);
+    }
+    a.A = zeros<S, NX, NX>();
+    a.b = x;
+    a.C = P;
+    a.eta = zeros<S, NX, 1>();
+    a.J = zeros<S, NX, NX>();
+  } else {
+    a = make_filter_elem<S, NX, NY>(m, k0, e);
+    for (long long k = k0 + 1; k < k1; ++k) {
+      // predict the conditional: (F A, F b + u, F C F^T + Q)
+      const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
+      const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
+      const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
+      a.A = mul(F, a.A);
+      a.b = mul_add(F, a.b, u);
+      const Mat<S, NX, NX> fc = mul(F, a.C);
+      a.C = mul_nt_sym_add(fc, F, Q);
+      cond_update(a, load_meas<S, NX, NY>(m, k), e);
+    }
+  }
+  fe_store(agg, cap, c, a);
+  if (e) atomicOr(err, e);
+}
+
+// finish: sequential Kalman filter over the chunk from the carried prefix
+// (inclusive prefix of chunk c-1 = filtered state at step c L - 1)
+template <typename S, int NX, int NY>
+__global__ void __launch_bounds__(128)
+    k_filter_finish(ModelView<S> m, long long L, long long nchunks,
+                    const S* pre, long long pre_cap, S* mean, S* cov,
+                    unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  Vec<S, NX> x;
+  Mat<S, NX, NX> P;
+  if (c == 0) {
+    x = load<S, NX, 1>(m.m0);
+    P = load<S, NX, NX>(m.p0);
+  } else {
+    x = load_soa<S, NX, 1>(pre + FLayout<NX>::b * pre_cap + (c - 1), pre_cap);
+    P = load_soa<S, NX, NX>(pre + FLayout<NX>::C * pre_cap + (c - 1), pre_cap);
+  }
+  for (long long k = k0; k < k1; ++k) {
+    kf_predict(x, P, m, k);
+    kf_update(x, P, load_meas<S, NX, NY>(m, k), e);
+    store_state(mean, cov, k, x, P);
+  }
+  if (e) atomicOr(err, e);
+}
+
+// ============================================================================
+// RTS smoother kernels (reverse direction)
+// ============================================================================
+
+// reduce: suffix element a_{k0} (x) ... (x) a_{k1-1} of the chunk
+template <typename S, int NX>
+__global__ void __launch_bounds__(128)
+    k_smoother_reduce(ModelView<S> m, const S* fmean, const S* fcov,
+                      long long L, long long nchunks, S* agg, long long cap,
+                      unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  Vec<S, NX> x;
+  Mat<S, NX, NX> P;
+  load_state(fmean, fcov, k1 - 1, x, P);
+  SElem<S, NX> a = make_smoother_elem(m, k1 - 1, x, P, e);
+  for (long long i = k1 - 2; i >= k0; --i) {
+    load_state(fmean, fcov, i, x, P);
+    const SElem<S, NX> ei = make_smoother_elem(m, i, x, P, e);
+    a = smoother_combine(ei, a);
+  }
+  se_store(agg, cap, c, a);
+  if (e) atomicOr(err, e);
+}
+
+// finish: sequential RTS over the chunk from the carried suffix (the
+// inclusive reversed prefix of chunk c+1 = smoothed state at step k1)
+template <typename S, int NX>
+__global__ void __launch_bounds__(128)
+    k_smoother_finish(ModelView<S> m, long long L, long long nchunks,
+                      const S* suf, long long suf_cap, S* mean, S* cov,
+                      unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  Vec<S, NX> gs;
+  Mat<S, NX, NX> Ls;
+  if (c + 1 < nchunks) {
+    gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + (c + 1), suf_cap);
+    Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + (c + 1), suf_cap);
+  }
+  // `mean`/`cov` hold the filtered stats on entry (in place: each step is
+  // read before it is overwritten by the same thread)
+  for (long long i = k1 - 1; i >= k0; --i) {
+    Vec<S, NX> x;
+    Mat<S, NX, NX> P;
+    load_state(mean, cov, i, x, P);
+    if (i == m.t - 1) {
+      gs = x;
+      Ls = P;
+    } else {
+      const SElem<S, NX> ei = make_smoother_elem(m, i, x, P, e);
+      gs = mul_add(ei.E, gs, ei.g);
+      const Mat<S, NX, NX> el = mul(ei.E, Ls);
+      Ls = mul_nt_sym_add(el, ei.E, ei.L);
+    }
+    store_state(mean, cov, i, gs, Ls);
+  }
+  if (e) atomicOr(err, e);
+}
+
+// ============================================================================
+// Two-filter smoother: backward (shifted) filter + combination (K8)
+// ============================================================================
+
+// reduce: slots [k0, k1) hold a_{i+2} (0-based step i+1) or the identity
+// (build_shifted_filter_elems, kalman_par.hpp:63-89); the chunk element is
+// their ordered product.
+template <typename S, int NX, int NY>
+__global__ void __launch_bounds__(128)
+    k_bwd_reduce(ModelView<S> m, long long L, long long nchunks, S* agg,
+                 long long cap, unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  // slots with i + 1 <= T - 1 carry an element
+  const long long last = min(k1, m.t - 1);  // exclusive end of real slots
+  FElem<S, NX> a;
+  if (last <= k0) {
+    a = fe_identity<S, NX>();
+  } else {
+    a = make_filter_elem<S, NX, NY>(m, last, e);  // slot last-1 -> step last
+    for (long long i = last - 2; i >= k0; --i) {
+      const FElem<S, NX> ei = make_filter_elem<S, NX, NY>(m, i + 1, e);
+      a = filter_combine(ei, a, e);
+    }
+  }
+  fe_store(agg, cap, c, a);
+  if (e) atomicOr(err, e);
+}
+
+// finish: backward information recursion (eta, J) <- a (x) (eta, J) over the
+// chunk, fused with tf_combine (kalman_seq.hpp:236-260) against the filtered
+// stats held in mean/cov (overwritten in place with the smoothed stats).
+template <typename S, int NX, int NY>
+__global__ void __launch_bounds__(128)
+    k_bwd_finish(ModelView<S> m, long long L, long long nchunks, const S* suf,
+                 long long suf_cap, S* mean, S* cov, unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  Vec<S, NX> eta = zeros<S, NX, 1>();
+  Mat<S, NX, NX> J = zeros<S, NX, NX>();
+  if (c + 1 < nchunks) {
+    eta = load_soa<S, NX, 1>(suf + FLayout<NX>::eta * suf_cap + (c + 1), suf_cap);
+    J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + (c + 1), suf_cap);
+  }
+  for (long long i = k1 - 1; i >= k0; --i) {
+    if (i + 1 <= m.t - 1) {
+      // (eta, J) of a (x) s for the element a of step i+1 (Lemma 1, eta/J
+      // rows only: they depend on the right operand through (eta, J) alone)
+      const FElem<S, NX> a = make_filter_elem<S, NX, NY>(m, i + 1, e);
+      Mat<S, NX, NX> nm = mul(J, a.C);  // N = I + J_s C_a
+#pragma unroll
+      for (int q = 0; q < NX; ++q) nm.a[q][q] += S(1);
+      const LU<S, NX> lu = lu_factor(nm, e);
+      const Vec<S, NX> w = sub_mul(eta, J, a.b);
+      const Vec<S, NX> y = lu_solve(lu, w);
+      const Mat<S, NX, NX> yj = lu_solve(lu, J);
+      const Mat<S, NX, NX> v = mul(yj, a.A);
+      eta = mul_tn_add(a.A, y, a.eta);
+      J = mul_tn_sym_add(a.A, v, a.J);
+    }
+    // two-filter combination: (I + P J)^-1 (x + P eta), (I + P J)^-1 P
+    Vec<S, NX> x;
+    Mat<S, NX, NX> P;
+    load_state(mean, cov, i, x, P);
+    Mat<S, NX, NX> mm = mul(P, J);
+#pragma unroll
+    for (int q = 0; q < NX; ++q) mm.a[q][q] += S(1);
+    const LU<S, NX> lu = lu_factor(mm, e);
+    const Vec<S, NX> rhs = mul_add(P, eta, x);
+    const Vec<S, NX> xs = lu_solve(lu, rhs);
+    Mat<S, NX, NX> ps = lu_solve(lu, P);
+    symmetrize(ps);
+    store_state(mean, cov, i, xs, ps);
+  }
+  if (e) atomicOr(err, e);
+}
+
+// padding slots [from, to) <- identity
+template <class Ops>
+__global__ void k_fill_identity(Ops ops, ElemBuf<typename Ops::S> b,
+                                long long from, long long to) {
+  const long long i = from + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < to) ops.identity(b, i);
+}
+
+}  // namespace psk
