@@ -72,6 +72,9 @@ class Oracle:
             raise FileNotFoundError(f"{path} not built (make -C oracle)")
         self.lib = C.CDLL(str(path))
         self.pre = "pso_" if which == "port" else "psr_"
+        if which == "port":
+            for n in ("pso_last_scan_work", "pso_last_scan_span", "pso_splitmix64"):
+                getattr(self.lib, n).restype = C.c_uint64
 
     # -- helpers -----------------------------------------------------------
     def _fn(self, name: str, sfx: str | None = None):

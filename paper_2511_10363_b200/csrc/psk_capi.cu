@@ -231,7 +231,8 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
 
 int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
               uint64_t sengupta_n, void* mean, void* cov) {
-  if (!ctx) return fail(PSK_E_ARG, "null context");
+  // argument and contract validation first (host-only, no device needed),
+  // then the context
   if (!m) return fail(PSK_E_ARG, "null model");
   if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16)
     return fail(PSK_E_DIM, "mat dims");  // Mat requires 1..kMaxDim (mat.hpp:19, 326)
@@ -240,6 +241,7 @@ int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
   int st = check_contract(alg, sengupta_n, m->t);
   if (st) return st;
   if (m->t > 0 && (!mean || !cov)) return fail(PSK_E_ARG, "null output");
+  if (!ctx) return fail(PSK_E_ARG, "null context");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard dg(ctx->device);
   ctx->launch.stream = ctx->stream;
