@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: filter + RTS smoother time-steps/s (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3] at N=1): T = 2^24 steps, nx = 4, ny = 2,
+FP64, the stationary damped constant-velocity tracking model written per step
+(time-varying layout, the reference API is per step), PRTS with the
+single-pass decoupled look-back scan.  One "step" of the benchmark is one full
+prts_run over the whole series.
+
+  value  -- device-resident throughput: inputs already in HBM, outputs to HBM,
+            CUDA events on the library's stream, max over ranks;
+  e2e    -- the same call through the public API with pinned HOST buffers:
+            H2D of all inputs and D2H of all outputs inside the timed region.
+
+With --gpus N > 1 (torchrun, one rank per GPU) the time axis is sharded: each
+rank filters / smooths its contiguous chunk, the shard aggregates are
+exchanged with an NCCL all_gather and folded (paper_2511_10363_b200/
+distributed.py); scaling is "strong" (T fixed).
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libparascan_ref.so: prts_run with PoolBackend on all host
+threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": HBM_FALLBACK, "src": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8
+                          for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# algorithmic HBM bytes per time step for each fast-path kernel (nx=4, ny=2;
+# DESIGN.md section 4): inputs 52 scalars, filtered/smoothed stats 20 scalars,
+# smoother inputs (filtered 20 + F,Q,u of the next step 36)
+def kernel_bytes_per_step(nx: int, ny: int, s: int) -> dict:
+    inp = nx * nx * 2 + nx + ny * nx + ny + ny * ny + ny
+    st = nx + nx * nx
+    sm_in = st + 2 * nx * nx + nx
+    return {"filter_reduce": inp * s, "filter_finish": (inp + st) * s,
+            "smoother_reduce": sm_in * s, "smoother_finish": (sm_in + st) * s}
+
+
+def cpu_reference(T_sample: int, threads: int, runs: int, seed: int = 0) -> dict:
+    """The reference's own CPU path on the same workload (bounded sample)."""
+    from oracle.oracle import Oracle  # baseline leg only
+    from paper_2511_10363_b200.synthetic import cv_model
+
+    m, ys = cv_model(T_sample, seed=seed)
+    h = Oracle("ref").time_handle(m, ys)
+    h.time("prts", 3, 16, threads)  # warm-up
+    ts = [h.time("prts", 3, 16, threads) for _ in range(runs)]
+    seq = [h.time("seq", 3, 16, 1) for _ in range(max(1, runs // 2))]
+    return {"value": T_sample * len(ts) / sum(ts), "unit": "time-steps/s",
+            "cores": threads, "kind": "reference",
+            "sample": f"prts_run InplaceLaFi PoolBackend({threads}) on the first "
+                      f"T={T_sample} steps of the same damped-CV f64 workload, "
+                      f"{runs} runs",
+            "sequential_kf_rts_1core": T_sample * len(seq) / sum(seq)}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    T_sample = 1 << args.ref_log2t
+    from oracle.oracle import Oracle
+    from paper_2511_10363_b200.synthetic import cv_model
+
+    m, ys = cv_model(T_sample, seed=0)
+    h = Oracle("ref").time_handle(m, ys)
+    for _ in range(args.warmup):
+        h.time("prts", 3, 16, threads)
+    ts = [h.time("prts", 3, 16, threads) for _ in range(args.steps)]
+    value = T_sample * len(ts) / sum(ts)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "time-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args, note=f"reference CPU sample T={T_sample}"),
+        "cpu_baseline": {"value": value, "unit": "time-steps/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"prts_run InplaceLaFi PoolBackend({threads}), "
+                                   f"T={T_sample} per step"},
+        "e2e": {"value": value, "unit": "time-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "time-steps/sec filter+smoother (PRTS) vs T, % of HBM roofline"
+
+
+def config(args, note: str | None = None) -> dict:
+    c = {"workload": f"PRTS T=2^{args.log2t} nx=4 ny=2 damped constant-velocity tracking "
+                     f"(BASELINE configs[3] at N={args.gpus})",
+         "T": 1 << args.log2t, "nx": 4, "ny": 2, "alg": args.alg, "chunk": args.chunk,
+         "layout": "per-step (time-varying) model arrays" if not args.broadcast
+                   else "time-invariant (broadcast) model, streamed y",
+         "l2": "no flush needed: per-step inputs (7.0 GB f64) >> 126 MB L2",
+         "parallelism": f"time-sharded x{args.gpus}" if args.gpus > 1 else "single GPU"}
+    if note:
+        c["note"] = note
+    return c
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="psk", choices=["psk", "reference"])
+    ap.add_argument("--log2t", type=int, default=24)
+    ap.add_argument("--alg", default="DecoupledLookback")
+    ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--broadcast", action="store_true")
+    ap.add_argument("--ref-log2t", type=int, default=18)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    run_psk(args)
+
+
+def run_psk(args) -> None:
+    import torch
+
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200 import distributed as dist_psk
+    from paper_2511_10363_b200.synthetic import cv_matrices, simulate_cv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    T = 1 << args.log2t
+    f64 = args.dtype == "f64"
+    tdt = torch.float64 if f64 else torch.float32
+    S = 8 if f64 else 4
+    nx, ny = 4, 2
+
+    # ---- synthetic inputs (same series on every rank; each rank keeps its shard)
+    F, Q, H, R, m0, P0 = cv_matrices()
+    ys_np = simulate_cv(T, seed=0)
+    lo, hi = dist_psk.shard_range(T, rank, world)
+    hi_in = min(hi + 1, T)  # one extra transition for the smoother boundary
+
+    def field(a, n):
+        t = torch.as_tensor(a, dtype=tdt, device=dev)
+        if args.broadcast:
+            return t
+        return t.expand(n, *t.shape).contiguous()
+
+    n_in = hi_in - lo
+    model = psk.Lgssm(f=field(F, n_in), u=field(np.zeros(4), n_in), q=field(Q, n_in),
+                      h=field(H, n_in), d=field(np.zeros(2), n_in), r=field(R, n_in),
+                      prior_mean=torch.as_tensor(m0, dtype=tdt, device=dev),
+                      prior_cov=torch.as_tensor(P0, dtype=tdt, device=dev), t=n_in)
+    ys = torch.as_tensor(ys_np[lo:hi_in], dtype=tdt, device=dev)
+    spec = psk.ScanSpec(psk.ScanAlg[args.alg], 16)
+    stream = torch.cuda.Stream(device=dev)
+    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk, stream=stream)
+
+    def step(profile: bool = False):
+        be.set_profile(profile)
+        with torch.cuda.stream(stream):
+            out = dist_psk.prts_run_sharded(model, ys, spec, be, rank, world, lo, hi, T, pg)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg is not None:
+        torch.distributed.barrier()
+    launches = 0
+    prof: dict[str, list[float]] = {}
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(profile=True)
+            launches += be.last_launch_count()
+            for name, ms in be.last_profile():
+                prof.setdefault(name, []).append(ms)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if pg is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = T / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (per-launch averages, this run)
+    peaks = _peaks()
+    bps = kernel_bytes_per_step(nx, ny, S)
+    per_kernel = {k: (sum(v) / len(v), len(v)) for k, v in prof.items()}
+    totals = {k: sum(v) for k, v in prof.items()}
+    dom = max(totals, key=totals.get) if totals else None
+    if dom not in bps and totals:  # dominant kernel with an HBM byte model
+        dom = max((k for k in totals if k in bps), key=totals.get, default=None)
+    steps_local = hi - lo
+    roof = None
+    if dom in bps:
+        avg_ms = per_kernel[dom][0]
+        gbs = bps[dom] * steps_local / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(gbs, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
+                "traffic": None, "peak_source": peaks["src"],
+                "bytes_per_step": bps[dom], "avg_ms": round(avg_ms, 4)}
+    kernels = {k: {"avg_ms": round(v[0], 4), "launches_per_step": v[1] // args.steps,
+                   "share": round(totals[k] / sum(totals.values()), 4)}
+               for k, v in per_kernel.items()}
+    for k in kernels:
+        if k in bps:
+            kernels[k]["GBps"] = round(bps[k] * steps_local / (kernels[k]["avg_ms"] * 1e-3) / 1e9, 1)
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local)
+
+    # ---- CPU baseline (reference CPU path, rank 0, N=1 only)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        try:
+            cpu = cpu_reference(1 << args.ref_log2t, os.cpu_count() or 1, runs=8)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic", "config": config(args),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
+    import torch
+
+    def pinned(a, n=None):
+        t = torch.as_tensor(a, dtype=tdt)
+        if n is not None and not args.broadcast:
+            t = t.expand(n, *t.shape)
+        out = torch.empty(t.shape, dtype=tdt, pin_memory=True)
+        out.copy_(t)
+        return out
+
+    m = psk.Lgssm(f=pinned(F, T), u=pinned(np.zeros(4), T), q=pinned(Q, T),
+                  h=pinned(H, T), d=pinned(np.zeros(2), T), r=pinned(R, T),
+                  prior_mean=pinned(m0), prior_cov=pinned(P0), t=T)
+    ys = pinned(ys_np)
+    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk)
+    h2d = sum(a.numel() * a.element_size() for a in (m.f, m.u, m.q, m.h, m.d, m.r, ys,
+                                                     m.prior_mean, m.prior_cov))
+    d2h = T * 20 * (8 if tdt == torch.float64 else 4)
+    # pinned outputs, reused across steps (the API call fills them)
+    res = psk.GaussianStats(torch.empty((T, 4), dtype=tdt, pin_memory=True),
+                            torch.empty((T, 4, 4), dtype=tdt, pin_memory=True))
+    psk.prts_run(m, ys, spec, be, out=res)  # warm-up
+    ts = []
+    steps = max(1, min(args.steps, 5))
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = psk.prts_run(m, ys, spec, be, out=res)
+        float(out.mean[-1, 0])  # the result is on the host
+        ts.append(time.perf_counter() - t0)
+    sec = sum(ts) / len(ts)
+    return {"value": T / sec, "unit": "time-steps/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "timer": "wall clock around the synchronous API call"}
+
+
+if __name__ == "__main__":
+    main()

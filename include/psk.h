@@ -117,6 +117,46 @@ int psk_ptfs(psk_ctx* ctx_fwd, psk_ctx* ctx_bwd, int devices,
              const psk_model* model, int alg, uint64_t sengupta_n, void* mean,
              void* cov);
 
+/* ---- time-sharded PRTS: one process per GPU (paper_2511_10363_b200/
+ * distributed.py).  A shard is the steps [lo, hi) of a
+ * T-step series, passed as a DEVICE-space psk_model with t = hi - lo.  Unless
+ * the shard contains step T-1, its f/u/q arrays carry one more transition at
+ * local index t (needed by the smoother element of step hi-1).
+ *   flags: PSK_SHARD_FIRST  lo == 0 (the first step absorbs the prior)
+ *          PSK_SHARD_LAST   hi == T
+ * Element and state buffers are device arrays in model->dtype:
+ *   filter element    3 nx^2 + 2 nx scalars (A | b | C | eta | J), row-major
+ *   smoother element  2 nx^2 + nx   scalars (E | g | L)
+ *   state             nx + nx^2     scalars (mean | cov)
+ * A reduce call leaves the shard's scanned chunk elements in the context for
+ * the following finish call.  The only cross-GPU data are the shard elements
+ * (gathered by the caller, e.g. an NCCL all_gather) and their folds. */
+#define PSK_SHARD_FIRST 1
+#define PSK_SHARD_LAST 2
+/* filter pass, part 1: local element build + scan; elem_out = shard total */
+int psk_shard_filter_reduce(psk_ctx* ctx, const psk_model* shard, int flags,
+                            int alg, uint64_t sengupta_n, void* elem_out);
+/* filter pass, part 2: filtered stats of the shard from carry_state (the
+ * filtered state before the shard; NULL for the FIRST shard) */
+int psk_shard_filter_finish(psk_ctx* ctx, const psk_model* shard, int flags,
+                            const void* carry_state, void* mean, void* cov);
+/* smoother pass, part 1: mean/cov hold the shard's filtered stats;
+ * elem_out = the shard's suffix smoothing element */
+int psk_shard_smoother_reduce(psk_ctx* ctx, const psk_model* shard, int flags,
+                              int alg, uint64_t sengupta_n, const void* mean,
+                              const void* cov, void* elem_out);
+/* smoother pass, part 2: smoothed stats written in place over mean/cov from
+ * carry_state (the smoothed state after the shard; NULL for the LAST shard) */
+int psk_shard_smoother_finish(psk_ctx* ctx, const psk_model* shard, int flags,
+                              const void* carry_state, void* mean, void* cov);
+/* prefix fold e_0 (x) ... (x) e_{count-1} of gathered filter elements (the
+ * first contains a_1) -> filtered state; suffix fold of smoother elements
+ * (the last contains a_T) -> smoothed state.  Device buffers, on ctx. */
+int psk_fold_filter(psk_ctx* ctx, int dtype, int nx, const void* elems,
+                    int count, void* state_out);
+int psk_fold_smoother(psk_ctx* ctx, int dtype, int nx, const void* elems,
+                      int count, void* state_out);
+
 /* Per-kernel device time of the last call, for roofline accounting:
  * fills up to `cap` entries of names[i] (static strings) / ms[i]; returns
  * the number of recorded kernels (recording enabled by psk_set_profile). */

@@ -17,6 +17,7 @@ PSK_E_CUDA, PSK_E_NCCL, PSK_E_ARG, PSK_E_ALLOC = 5, 6, 7, 8
 PSK_F32, PSK_F64 = 0, 1
 PSK_HOST, PSK_DEVICE = 0, 1
 PSK_MODE_FAST, PSK_MODE_EXACT = 0, 1
+PSK_SHARD_FIRST, PSK_SHARD_LAST = 1, 2
 
 
 class psk_model(C.Structure):
@@ -51,6 +52,19 @@ SIGNATURES = {
                            C.c_void_p, C.c_void_p]),
     "psk_ptfs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(psk_model),
                            C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "psk_shard_filter_reduce": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                          C.c_int, C.c_uint64, C.c_void_p]),
+    "psk_shard_filter_finish": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]),
+    "psk_shard_smoother_reduce": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                            C.c_int, C.c_uint64, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]),
+    "psk_shard_smoother_finish": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                            C.c_void_p, C.c_void_p, C.c_void_p]),
+    "psk_fold_filter": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                  C.c_void_p]),
+    "psk_fold_smoother": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_void_p]),
     "psk_set_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "psk_last_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p),
                                    C.POINTER(C.c_float), C.c_int]),

@@ -327,10 +327,16 @@ def _validate(m: Lgssm) -> None:
 
 
 def _run(entry: str, m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,
-         be_bwd: CudaBackend | None = None, devices: int = 1) -> GaussianStats:
+         be_bwd: CudaBackend | None = None, devices: int = 1,
+         out: GaussianStats | None = None) -> GaussianStats:
     _validate(m)
     mk = _Marshal(m, ys)
-    mean, cov = mk.outputs()
+    if out is None:
+        mean, cov = mk.outputs()
+    else:  # caller-provided buffers (e.g. pinned host memory), same kind as inputs
+        mean, cov = out.mean, out.cov
+        if tuple(mean.shape) != (mk.t, mk.nx) or tuple(cov.shape) != (mk.t, mk.nx, mk.nx):
+            raise DimensionMismatch("output buffer shapes")
     L = _lib.lib()
     pm = C.c_void_p(mk._ptr(mean))
     pc = C.c_void_p(mk._ptr(cov))
@@ -345,17 +351,20 @@ def _run(entry: str, m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,
     return GaussianStats(mean, cov)
 
 
-def pkf_run(m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend) -> GaussianStats:
+def pkf_run(m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,
+            out: GaussianStats | None = None) -> GaussianStats:
     """Parallel Kalman filter, Alg. 5 (kalman_par.hpp:111-119)."""
-    return _run("pkf", m, ys, spec, be)
+    return _run("pkf", m, ys, spec, be, out=out)
 
 
-def prts_run(m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend) -> GaussianStats:
+def prts_run(m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,
+             out: GaussianStats | None = None) -> GaussianStats:
     """Parallel RTS smoother, Alg. 6 (kalman_par.hpp:156-179)."""
-    return _run("prts", m, ys, spec, be)
+    return _run("prts", m, ys, spec, be, out=out)
 
 
 def ptfs_run(m: Lgssm, ys: Any, spec: ScanSpec, be_fwd: CudaBackend,
-             be_bwd: CudaBackend | None = None, devices: int = 1) -> GaussianStats:
+             be_bwd: CudaBackend | None = None, devices: int = 1,
+             out: GaussianStats | None = None) -> GaussianStats:
     """Parallel two-filter smoother, Alg. 7 (kalman_par.hpp:207-238)."""
-    return _run("ptfs", m, ys, spec, be_fwd, be_bwd, devices)
+    return _run("ptfs", m, ys, spec, be_fwd, be_bwd, devices, out=out)

@@ -70,6 +70,13 @@ def build(verbose: bool = False) -> Path:
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}{p.stderr}")
+    tools = LIB / "libpsk_tools.so"
+    src = CSRC / "psk_peak.cu"
+    if not tools.exists() or src.stat().st_mtime > tools.stat().st_mtime:
+        cmd = [NVCC, *COMMON, "-shared", "-o", str(tools), str(src)]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"tools build failed:\n{p.stdout}{p.stderr}")
     return out
 
 

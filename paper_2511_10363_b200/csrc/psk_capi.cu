@@ -40,7 +40,10 @@ struct psk_ctx {
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
-  std::vector<void*> allocs;  // per-call device allocations
+  std::vector<void*> allocs;   // per-call device allocations
+  std::vector<void*> persist;  // sharded-run scratch kept between calls
+  void* shard_scratch = nullptr;
+  int shard_dtype = -1;
   std::vector<std::pair<const char*, float>> profile;
 };
 
@@ -71,6 +74,18 @@ void ctx_free_all(psk_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFreeAsync(p, ctx->stream);
   ctx->allocs.clear();
 }
+void* ctx_alloc_persist(size_t bytes, void* c) {
+  psk_ctx* ctx = static_cast<psk_ctx*>(c);
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) return nullptr;
+  ctx->persist.push_back(p);
+  return p;
+}
+void ctx_free_persist(psk_ctx* ctx) {
+  for (void* p : ctx->persist) cudaFreeAsync(p, ctx->stream);
+  ctx->persist.clear();
+}
 
 inline bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
@@ -88,7 +103,7 @@ struct Field {
 // when 16-byte aligned, host (or misaligned) inputs are packed into dense
 // device arrays (time-invariant fields keep a single block, stride 0).
 template <typename S>
-int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v) {
+int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_fuq = 0) {
   const long long T = (long long)m->t;
   const int nx = m->nx, ny = m->ny;
   Field f[7] = {{m->f, m->f_stride, (long long)nx * nx, "f"},
@@ -115,8 +130,10 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v) {
       outs[i] = st;
       continue;
     }
-    // pack: one block if broadcast, else T blocks at the given stride
-    const long long nblk = st == 0 ? 1 : (T > 0 ? T : 1);
+    // pack: one block if broadcast, else T blocks at the given stride (plus the
+    // boundary transition of a sharded run for f/u/q)
+    const long long nblk =
+        st == 0 ? 1 : (T > 0 ? T : 1) + ((i == 0 || i == 1 || i == 2) ? extra_fuq : 0);
     S* dst = static_cast<S*>(ctx_alloc(sizeof(S) * (size_t)(nblk * f[i].block), ctx));
     if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
     const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
@@ -155,6 +172,8 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v) {
   v.t = T;
   v.nx = nx;
   v.ny = ny;
+  v.prior_first = 1;
+  v.last_step = T - 1;
   return PSK_OK;
 }
 
@@ -269,6 +288,119 @@ int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
   return PSK_OK;
 }
 
+// ---- time-sharded phases --------------------------------------------------
+template <typename S>
+int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
+                uint64_t sn, void* mean, void* cov, const void* carry, void* elem_out) {
+  ModelView<S> v;
+  const int extra = (flags & PSK_SHARD_LAST) ? 0 : 1;
+  int st = prepare_model<S>(ctx, m, v, extra);
+  if (st) return st;
+  v.prior_first = (flags & PSK_SHARD_FIRST) ? 1 : 0;
+  v.last_step = (flags & PSK_SHARD_LAST) ? (long long)m->t - 1 : -1;
+  FastArgs a;
+  a.method = 1;
+  a.alg = alg;
+  a.sengupta_n = sn;
+  a.chunk = ctx->chunk;
+  if (phase == 0 || phase == 2) {
+    ctx_free_persist(ctx);
+    if (ctx->shard_scratch) {
+      if (ctx->shard_dtype == PSK_F64) fast_shard_release<double>(ctx->shard_scratch);
+      else fast_shard_release<float>(ctx->shard_scratch);
+      ctx->shard_scratch = nullptr;
+    }
+    ctx->shard_dtype = m->dtype;
+  } else if (!ctx->shard_scratch || ctx->shard_dtype != m->dtype) {
+    return fail(PSK_E_ARG, "finish without a matching reduce on this context");
+  }
+  st = fast_shard_phase<S>(ctx->launch, v, a, phase, &ctx->shard_scratch,
+                           static_cast<S*>(mean), static_cast<S*>(cov),
+                           static_cast<const S*>(carry), static_cast<S*>(elem_out),
+                           ctx_alloc_persist, ctx);
+  if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
+  if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (shard scan)");
+  if (st) return fail(PSK_E_CUDA, "shard phase failed");
+  return PSK_OK;
+}
+
+int finish_call(psk_ctx* ctx, int st) {
+  unsigned herr = 0;
+  cudaMemcpyAsync(&herr, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+  ctx_free_all(ctx);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+  ctx->profile.clear();
+  if (ctx->launch.profile && ctx->launch.evs.size() > 1) {
+    for (size_t i = 0; i + 1 < ctx->launch.evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->launch.evs[i], ctx->launch.evs[i + 1]);
+      ctx->profile.emplace_back(ctx->launch.names[i], ms);
+    }
+  }
+  if (herr & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
+  return PSK_OK;
+}
+
+int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg, uint64_t sn,
+                void* mean, void* cov, const void* carry, void* elem_out) {
+  if (!m) return fail(PSK_E_ARG, "null model");
+  if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16) return fail(PSK_E_DIM, "mat dims");
+  if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+  if (m->space != PSK_DEVICE) return fail(PSK_E_ARG, "sharded runs take device-space shards");
+  if (phase == 0 || phase == 2) {
+    int st = check_contract(alg, sn, m->t);
+    if (st) return st;
+  }
+  if (m->t == 0) return fail(PSK_E_CONTRACT, "empty shard");
+  if (!mean || !cov) return fail(PSK_E_ARG, "null stats buffer");
+  if ((phase == 0 || phase == 2) && !elem_out) return fail(PSK_E_ARG, "null element output");
+  if (phase == 1 && !(flags & PSK_SHARD_FIRST) && !carry)
+    return fail(PSK_E_ARG, "non-first shard needs the carried filtered state");
+  if (phase == 3 && !(flags & PSK_SHARD_LAST) && !carry)
+    return fail(PSK_E_ARG, "non-last shard needs the carried smoothed state");
+  if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (ctx->mode != PSK_MODE_FAST) return fail(PSK_E_ARG, "sharded runs use the fast path");
+  const bool ok = m->dtype == PSK_F64 ? fast_supported<double>(m->nx, m->ny)
+                                      : fast_supported<float>(m->nx, m->ny);
+  if (!ok) return fail(PSK_E_DIM, "no fast-path instantiation for these dimensions");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg(ctx->device);
+  ctx->launch.stream = ctx->stream;
+  ctx->launch.err = ctx->d_err;
+  ctx->launch.start();
+  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  int st = m->dtype == PSK_F64
+               ? shard_typed<double>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out)
+               : shard_typed<float>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out);
+  return finish_call(ctx, st);
+}
+
+int fold_entry(psk_ctx* ctx, int kind, int dtype, int nx, const void* elems, int count,
+               void* out) {
+  if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (dtype != PSK_F32 && dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+  if (!elems || !out || count < 1) return fail(PSK_E_ARG, "bad fold arguments");
+  if (nx < 1 || nx > 4) return fail(PSK_E_DIM, "fold supports nx 1..4");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg(ctx->device);
+  ctx->launch.stream = ctx->stream;
+  ctx->launch.err = ctx->d_err;
+  ctx->launch.start();
+  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  int st = dtype == PSK_F64
+               ? fast_fold<double>(ctx->launch, kind, nx, static_cast<const double*>(elems),
+                                   count, static_cast<double*>(out))
+               : fast_fold<float>(ctx->launch, kind, nx, static_cast<const float*>(elems),
+                                  count, static_cast<float*>(out));
+  if (st) st = fail(PSK_E_ARG, "fold failed");
+  return finish_call(ctx, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -304,6 +436,11 @@ int psk_destroy(psk_ctx* c) {
   if (!c) return PSK_OK;
   {
     DeviceGuard dg(c->device);
+    ctx_free_persist(c);
+    if (c->shard_scratch) {
+      if (c->shard_dtype == PSK_F64) fast_shard_release<double>(c->shard_scratch);
+      else fast_shard_release<float>(c->shard_scratch);
+    }
     cudaStreamSynchronize(c->stream);
     c->launch.start();  // releases events
     cudaFree(c->d_err);
@@ -366,6 +503,32 @@ int psk_ptfs(psk_ctx* cf, psk_ctx* cb, int devices, const psk_model* m, int alg,
   // for any placement, test_kalman_par.cpp:209-227).
   (void)cb;
   return run_entry(cf, m, 2, alg, sn, mean, cov);
+}
+
+int psk_shard_filter_reduce(psk_ctx* c, const psk_model* m, int flags, int alg, uint64_t sn,
+                            void* elem_out) {
+  // mean/cov are not touched by a reduce; pass the element buffer to pass
+  // the null checks
+  return shard_entry(c, m, flags, 0, alg, sn, elem_out, elem_out, nullptr, elem_out);
+}
+int psk_shard_filter_finish(psk_ctx* c, const psk_model* m, int flags, const void* carry,
+                            void* mean, void* cov) {
+  return shard_entry(c, m, flags, 1, 0, 1, mean, cov, carry, nullptr);
+}
+int psk_shard_smoother_reduce(psk_ctx* c, const psk_model* m, int flags, int alg, uint64_t sn,
+                              const void* mean, const void* cov, void* elem_out) {
+  return shard_entry(c, m, flags, 2, alg, sn, const_cast<void*>(mean), const_cast<void*>(cov),
+                     nullptr, elem_out);
+}
+int psk_shard_smoother_finish(psk_ctx* c, const psk_model* m, int flags, const void* carry,
+                              void* mean, void* cov) {
+  return shard_entry(c, m, flags, 3, 0, 1, mean, cov, carry, nullptr);
+}
+int psk_fold_filter(psk_ctx* c, int dtype, int nx, const void* elems, int count, void* out) {
+  return fold_entry(c, 0, dtype, nx, elems, count, out);
+}
+int psk_fold_smoother(psk_ctx* c, int dtype, int nx, const void* elems, int count, void* out) {
+  return fold_entry(c, 1, dtype, nx, elems, count, out);
 }
 
 const char* psk_last_error(void) { return g_last_error.c_str(); }

@@ -19,6 +19,12 @@ struct ModelView {
   const S *m0, *p0;
   long long t;
   int nx, ny;
+  // time sharding (paper_2511_10363_b200/distributed.py): local step 0
+  // absorbs the prior only in the first shard; `last_step` is the local index
+  // of the series' last step T-1 (-1 when this shard does not contain it, in
+  // which case f/u/q carry one extra transition at local index t)
+  int prior_first;
+  long long last_step;
   __device__ __forceinline__ const S* F(long long k) const { return f + k * sf; }
   __device__ __forceinline__ const S* U(long long k) const { return u + k * su; }
   __device__ __forceinline__ const S* Q(long long k) const { return q + k * sq; }

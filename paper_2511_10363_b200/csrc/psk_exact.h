@@ -61,4 +61,13 @@ template <typename S>
 int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
              S* mean, S* cov, void* (*alloc)(size_t, void*), void* alloc_ctx);
 
+template <typename S>
+int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
+                     void** scratch, S* mean, S* cov, const S* carry, S* elem_out,
+                     void* (*alloc)(size_t, void*), void* actx);
+template <typename S>
+void fast_shard_release(void* scratch);
+template <typename S>
+int fast_fold(ExactLaunch& L, int kind, int nx, const S* aggs, int count, S* out);
+
 }  // namespace psk

@@ -324,7 +324,7 @@ __device__ __forceinline__ SElem<S, NX> make_smoother_elem(
     const ModelView<S>& m, long long i, const Vec<S, NX>& x,
     const Mat<S, NX, NX>& P, unsigned& err) {
   SElem<S, NX> e;
-  if (i == m.t - 1) {
+  if (i == m.last_step) {  // a_T = (0, x_T, P_T), kalman_elems.hpp:158-163
     e.E = zeros<S, NX, NX>();
     e.g = x;
     e.L = P;
@@ -371,6 +371,25 @@ __device__ __forceinline__ void load_state(const S* mean, const S* cov,
   P = load<S, NX, NX>(cov + k * NX * NX);
 }
 
+// Reduced Lemma-1 combine of a filtered state (an element with A = 0,
+// b = x, C = P) with an element e:  M = I + P J_e,
+// x' = A_e M^-1 (x + P eta_e) + b_e,  P' = A_e M^-1 P A_e^T + C_e.
+template <typename S, int NX>
+__device__ __forceinline__ void filter_apply(Vec<S, NX>& x, Mat<S, NX, NX>& P,
+                                             const FElem<S, NX>& e,
+                                             unsigned& err) {
+  Mat<S, NX, NX> m = mul(P, e.J);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) m.a[i][i] += S(1);
+  const LU<S, NX> lu = lu_factor(m, err);
+  const Vec<S, NX> rb = mul_add(P, e.eta, x);
+  const Vec<S, NX> z = lu_solve(lu, rb);
+  const Mat<S, NX, NX> xc = lu_solve(lu, P);
+  x = mul_add(e.A, z, e.b);
+  const Mat<S, NX, NX> w = mul(e.A, xc);
+  P = mul_nt_sym_add(w, e.A, e.C);
+}
+
 // ============================================================================
 // Filter kernels
 // ============================================================================
@@ -386,7 +405,7 @@ __global__ void __launch_bounds__(128)
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, m.t);
   FElem<S, NX> a;
-  if (k0 == 0) {
+  if (k0 == 0 && m.prior_first) {
     // a_1 absorbs the prior (kalman_elems.hpp:68-96): A = 0 and the prefix
     // is the filtered state itself, so run the chunk in state form.
     Vec<S, NX> x = load<S, NX, 1>(m.m0);
@@ -419,12 +438,16 @@ __global__ void __launch_bounds__(128)
 }
 
 // finish: sequential Kalman filter over the chunk from the carried prefix
-// (inclusive prefix of chunk c-1 = filtered state at step c L - 1)
+// (inclusive prefix of chunk c-1 = filtered state at step c L - 1).  In a
+// time-sharded run `carry` holds the filtered state at the step before the
+// shard (the fold of the predecessor shards' elements): the incoming state of
+// chunk c > 0 is then carry (x) (local prefix of chunk c-1), the reduced
+// Lemma-1 combine of a state (A = 0) with an element.
 template <typename S, int NX, int NY>
 __global__ void __launch_bounds__(128)
     k_filter_finish(ModelView<S> m, long long L, long long nchunks,
-                    const S* pre, long long pre_cap, S* mean, S* cov,
-                    unsigned* err) {
+                    const S* pre, long long pre_cap, const S* carry, S* mean,
+                    S* cov, unsigned* err) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   unsigned e = 0;
@@ -433,11 +456,20 @@ __global__ void __launch_bounds__(128)
   Vec<S, NX> x;
   Mat<S, NX, NX> P;
   if (c == 0) {
-    x = load<S, NX, 1>(m.m0);
-    P = load<S, NX, NX>(m.p0);
-  } else {
+    if (m.prior_first) {
+      x = load<S, NX, 1>(m.m0);
+      P = load<S, NX, NX>(m.p0);
+    } else {
+      x = load<S, NX, 1>(carry);
+      P = load<S, NX, NX>(carry + NX);
+    }
+  } else if (carry == nullptr) {
     x = load_soa<S, NX, 1>(pre + FLayout<NX>::b * pre_cap + (c - 1), pre_cap);
     P = load_soa<S, NX, NX>(pre + FLayout<NX>::C * pre_cap + (c - 1), pre_cap);
+  } else {
+    x = load<S, NX, 1>(carry);
+    P = load<S, NX, NX>(carry + NX);
+    filter_apply(x, P, fe_load<S, NX>(pre, pre_cap, c - 1), e);
   }
   for (long long k = k0; k < k1; ++k) {
     kf_predict(x, P, m, k);
@@ -476,12 +508,15 @@ __global__ void __launch_bounds__(128)
 }
 
 // finish: sequential RTS over the chunk from the carried suffix (the
-// inclusive reversed prefix of chunk c+1 = smoothed state at step k1)
+// inclusive reversed prefix of chunk c+1 = smoothed state at step k1).  In a
+// time-sharded run `carry` holds the smoothed state at the step after the
+// shard (fold of the successor shards' elements, E = 0): the incoming state of
+// chunk c < nchunks-1 is (local suffix of chunk c+1) (x) carry.
 template <typename S, int NX>
 __global__ void __launch_bounds__(128)
     k_smoother_finish(ModelView<S> m, long long L, long long nchunks,
-                      const S* suf, long long suf_cap, S* mean, S* cov,
-                      unsigned* err) {
+                      const S* suf, long long suf_cap, const S* carry, S* mean,
+                      S* cov, unsigned* err) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   unsigned e = 0;
@@ -492,6 +527,18 @@ __global__ void __launch_bounds__(128)
   if (c + 1 < nchunks) {
     gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + (c + 1), suf_cap);
     Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + (c + 1), suf_cap);
+    if (carry != nullptr) {
+      const Mat<S, NX, NX> E =
+          load_soa<S, NX, NX>(suf + SLayout<NX>::E * suf_cap + (c + 1), suf_cap);
+      const Vec<S, NX> cg = load<S, NX, 1>(carry);
+      const Mat<S, NX, NX> cl = load<S, NX, NX>(carry + NX);
+      gs = mul_add(E, cg, gs);
+      const Mat<S, NX, NX> el = mul(E, cl);
+      Ls = mul_nt_sym_add(el, E, Ls);
+    }
+  } else if (carry != nullptr) {
+    gs = load<S, NX, 1>(carry);
+    Ls = load<S, NX, NX>(carry + NX);
   }
   // `mean`/`cov` hold the filtered stats on entry (in place: each step is
   // read before it is overwritten by the same thread)
@@ -499,7 +546,7 @@ __global__ void __launch_bounds__(128)
     Vec<S, NX> x;
     Mat<S, NX, NX> P;
     load_state(mean, cov, i, x, P);
-    if (i == m.t - 1) {
+    if (i == m.last_step) {
       gs = x;
       Ls = P;
     } else {
@@ -530,7 +577,7 @@ __global__ void __launch_bounds__(128)
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, m.t);
   // slots with i + 1 <= T - 1 carry an element
-  const long long last = min(k1, m.t - 1);  // exclusive end of real slots
+  const long long last = min(k1, m.last_step);  // exclusive end of real slots
   FElem<S, NX> a;
   if (last <= k0) {
     a = fe_identity<S, NX>();
@@ -564,7 +611,7 @@ __global__ void __launch_bounds__(128)
     J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + (c + 1), suf_cap);
   }
   for (long long i = k1 - 1; i >= k0; --i) {
-    if (i + 1 <= m.t - 1) {
+    if (i + 1 <= m.last_step) {
       // (eta, J) of a (x) s for the element a of step i+1 (Lemma 1, eta/J
       // rows only: they depend on the right operand through (eta, J) alone)
       const FElem<S, NX> a = make_filter_elem<S, NX, NY>(m, i + 1, e);
@@ -594,6 +641,41 @@ __global__ void __launch_bounds__(128)
     store_state(mean, cov, i, xs, ps);
   }
   if (e) atomicOr(err, e);
+}
+
+// one packed element (row-major fields, FLayout / SLayout order) from slot i
+// of an SoA buffer
+template <typename S>
+__global__ void k_extract_elem(const S* buf, long long cap, long long i, int size,
+                               S* out) {
+  for (int c = threadIdx.x; c < size; c += blockDim.x) out[c] = buf[c * cap + i];
+}
+
+// Fold of `count` packed filter elements, left to right (non-commutative);
+// the first contains a_1 (A = 0), so the result is a state: out = (b | C).
+template <typename S, int NX>
+__global__ void k_fold_filter(const S* aggs, int count, S* out, unsigned* err) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned e = 0;
+  constexpr int FS = FLayout<NX>::size;
+  FElem<S, NX> acc = fe_load<S, NX>(aggs, 1, 0);
+  for (int k = 1; k < count; ++k) acc = filter_combine(acc, fe_load<S, NX>(aggs + k * FS, 1, 0), e);
+  for (int i = 0; i < NX; ++i) out[i] = acc.b.a[i][0];
+  for (int i = 0; i < NX; ++i)
+    for (int j = 0; j < NX; ++j) out[NX + i * NX + j] = acc.C.a[i][j];
+  if (e) atomicOr(err, e);
+}
+// Fold of `count` packed smoother elements, left to right; the last contains
+// a_T (E = 0), so the result is a state: out = (g | L).
+template <typename S, int NX>
+__global__ void k_fold_smoother(const S* aggs, int count, S* out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  constexpr int SS = SLayout<NX>::size;
+  SElem<S, NX> acc = se_load<S, NX>(aggs + (count - 1) * SS, 1, 0);
+  for (int k = count - 2; k >= 0; --k) acc = smoother_combine(se_load<S, NX>(aggs + k * SS, 1, 0), acc);
+  for (int i = 0; i < NX; ++i) out[i] = acc.g.a[i][0];
+  for (int i = 0; i < NX; ++i)
+    for (int j = 0; j < NX; ++j) out[NX + i * NX + j] = acc.L.a[i][j];
 }
 
 // padding slots [from, to) <- identity

@@ -1,9 +1,14 @@
-// psk_fast_f32.cu -- float instantiations of the fast path (split per
-// dtype so the two halves compile in parallel).
+// psk_fast_f32.cu -- float instantiations of the fast path (split per dtype
+// so the two halves compile in parallel).
 #include "psk_fast_impl.cuh"
 
 namespace psk {
 template bool fast_supported<float>(int, int);
-template int fast_run<float>(ExactLaunch&, const ModelView<float>&, const FastArgs&,
-                          float*, float*, void* (*)(size_t, void*), void*);
+template int fast_run<float>(ExactLaunch&, const ModelView<float>&, const FastArgs&, float*, float*,
+                          void* (*)(size_t, void*), void*);
+template int fast_shard_phase<float>(ExactLaunch&, const ModelView<float>&, const FastArgs&, int,
+                                  void**, float*, float*, const float*, float*,
+                                  void* (*)(size_t, void*), void*);
+template void fast_shard_release<float>(void*);
+template int fast_fold<float>(ExactLaunch&, int, int, const float*, int, float*);
 }  // namespace psk

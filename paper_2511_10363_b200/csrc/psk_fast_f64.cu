@@ -1,9 +1,14 @@
-// psk_fast_f64.cu -- double instantiations of the fast path (split per
-// dtype so the two halves compile in parallel).
+// psk_fast_f64.cu -- double instantiations of the fast path (split per dtype
+// so the two halves compile in parallel).
 #include "psk_fast_impl.cuh"
 
 namespace psk {
 template bool fast_supported<double>(int, int);
-template int fast_run<double>(ExactLaunch&, const ModelView<double>&, const FastArgs&,
-                          double*, double*, void* (*)(size_t, void*), void*);
+template int fast_run<double>(ExactLaunch&, const ModelView<double>&, const FastArgs&, double*, double*,
+                          void* (*)(size_t, void*), void*);
+template int fast_shard_phase<double>(ExactLaunch&, const ModelView<double>&, const FastArgs&, int,
+                                  void**, double*, double*, const double*, double*,
+                                  void* (*)(size_t, void*), void*);
+template void fast_shard_release<double>(void*);
+template int fast_fold<double>(ExactLaunch&, int, int, const double*, int, double*);
 }  // namespace psk

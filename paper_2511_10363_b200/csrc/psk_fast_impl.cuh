@@ -1,5 +1,6 @@
-// psk_fast_impl.cuh -- host dispatch of the fast (chunked) path and its template
-// instantiations.  See psk_fast.cuh for the formulation.
+// psk_fast_impl.cuh -- host dispatch of the fast (chunked) path, split into
+// phases so that a time-sharded run (distributed.py) can exchange shard
+// aggregates between the reduce+scan and the finish of each pass.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -27,14 +28,14 @@ constexpr int kBlock = 128;
 // Scan of chunk elements: level-by-level plan (alg 0..5) or the single-pass
 // decoupled look-back (alg 6).  `buf` holds npad slots (identity padded).
 template <class Ops>
-static int chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
-                      typename Ops::S* buf, long long nchunks, long long npad,
-                      int rev, typename Ops::S* aux1, typename Ops::S* aux2,
-                      const ScanPlan& plan, void* dlb_state) {
+static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
+                       typename Ops::S* buf, long long nchunks, long long npad,
+                       int rev, typename Ops::S* aux1, typename Ops::S* aux2,
+                       const ScanPlan& plan, void* dlb_state) {
   using S = typename Ops::S;
   if (a.alg == 6) {
     dlb_scan<Ops>(L, ops, buf, nchunks, rev, aux1, dlb_state);
-    return 0;
+    return;
   }
   Bufs3<Ops> bufs;
   bufs.b[0] = ElemBuf<S>{buf, npad, npad, rev};
@@ -45,71 +46,125 @@ static int chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
     k_level<Ops><<<g, kBlock, 0, L.stream>>>(ops, bufs, d);
     L.count("chunk_scan_level");
   }
+}
+
+// Scratch of one fast run (allocated by fast_prepare).
+template <typename S>
+struct FastScratch {
+  long long nchunks = 0, npad = 0, chunk = 1;
+  ScanPlan plan;
+  S *agg = nullptr, *aux1 = nullptr, *aux2 = nullptr;
+  void* dlb = nullptr;
+};
+
+template <typename S, int NX>
+static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<S>& sc,
+                          void* (*alloc)(size_t, void*), void* actx) {
+  const long long T = m.t;
+  sc.chunk = a.chunk < 1 ? 1 : a.chunk;
+  sc.nchunks = T > 0 ? (T + sc.chunk - 1) / sc.chunk : 0;
+  const bool dlb = a.alg == 6;
+  sc.npad = (dlb || a.alg == 0) ? sc.nchunks : (long long)next_pow2(sc.nchunks);
+  if (!dlb && sc.npad > 0) {
+    sc.plan = make_scan_plan(a.alg, a.sengupta_n, sc.npad);
+    if (sc.plan.status) return sc.plan.status;
+  }
+  constexpr int FS = FLayout<NX>::size;
+  const long long a1 = dlb ? 0 : sc.plan.cap1, a2 = dlb ? 0 : sc.plan.cap2;
+  sc.agg = (S*)alloc(sizeof(S) * FS * (sc.npad ? sc.npad : 1), actx);
+  sc.aux1 = (S*)alloc(sizeof(S) * FS * (a1 ? a1 : 1), actx);
+  sc.aux2 = (S*)alloc(sizeof(S) * FS * (a2 ? a2 : 1), actx);
+  sc.dlb = dlb ? alloc(dlb_state_bytes<S, NX>(sc.nchunks), actx) : nullptr;
+  if (!sc.agg || !sc.aux1 || !sc.aux2 || (dlb && !sc.dlb)) return 8;
+  return 0;
+}
+
+// phase: 0 filter reduce+scan, 1 filter finish, 2 smoother reduce+scan,
+//        3 smoother finish, 4 backward (shifted) reduce+scan, 5 backward
+//        finish fused with the two-filter combination.
+// `carry` (device, state nx + nx^2) is the boundary state of a sharded run
+// (nullptr otherwise); `elem_out` (device, packed element) receives the local
+// total of a reduce phase when non-null.
+template <typename S, int NX, int NY>
+static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
+                        FastScratch<S>& sc, int phase, S* mean, S* cov, const S* carry,
+                        S* elem_out) {
+  if (sc.nchunks == 0) return 0;
+  const long long Lc = sc.chunk, nch = sc.nchunks, npad = sc.npad;
+  FastFilterOps<S, NX> fops{L.err};
+  FastSmootherOps<S, NX> sops{L.err};
+  const int g = blocks_for(nch, kBlock);
+  auto fill = [&](auto ops) {
+    if (npad > nch) {
+      k_fill_identity<<<blocks_for(npad - nch, kBlock), kBlock, 0, L.stream>>>(
+          ops, ElemBuf<S>{sc.agg, npad, npad, 0}, nch, npad);
+      L.count("fill_identity");
+    }
+  };
+  switch (phase) {
+    case 0:
+      k_filter_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, L.err);
+      L.count("filter_reduce");
+      fill(fops);
+      chunk_scan(L, fops, a, sc.agg, nch, npad, 0, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      if (elem_out) {
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, npad, nch - 1, FLayout<NX>::size, elem_out);
+        L.count("extract_elem");
+      }
+      break;
+    case 1:
+      k_filter_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, carry,
+                                                             mean, cov, L.err);
+      L.count("filter_finish");
+      break;
+    case 2:
+      k_smoother_reduce<S, NX><<<g, kBlock, 0, L.stream>>>(m, mean, cov, Lc, nch, sc.agg, npad,
+                                                           L.err);
+      L.count("smoother_reduce");
+      fill(sops);
+      chunk_scan(L, sops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      if (elem_out) {
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, npad, 0, SLayout<NX>::size, elem_out);
+        L.count("extract_elem");
+      }
+      break;
+    case 3:
+      k_smoother_finish<S, NX><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, carry,
+                                                           mean, cov, L.err);
+      L.count("smoother_finish");
+      break;
+    case 4:
+      k_bwd_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, L.err);
+      L.count("bwd_reduce");
+      fill(fops);
+      chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      break;
+    case 5:
+      k_bwd_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, mean, cov,
+                                                          L.err);
+      L.count("bwd_finish_tf_combine");
+      break;
+    default:
+      return 7;
+  }
   return 0;
 }
 
 template <typename S, int NX, int NY>
-static int fast_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
-                      S* mean, S* cov, void* (*alloc)(size_t, void*),
-                      void* actx) {
-  const long long T = m.t;
-  if (T == 0) return 0;
-  const long long Lc = a.chunk < 1 ? 1 : a.chunk;
-  const long long nchunks = (T + Lc - 1) / Lc;
-  const bool dlb = a.alg == 6;
-  const long long npad =
-      (dlb || a.alg == 0) ? nchunks : (long long)next_pow2(nchunks);
-  ScanPlan plan;
-  if (!dlb) {
-    plan = make_scan_plan(a.alg, a.sengupta_n, npad);
-    if (plan.status) return plan.status;
-  }
-  constexpr int FS = FLayout<NX>::size;
-  const long long aux1n = dlb ? 0 : plan.cap1, aux2n = dlb ? 0 : plan.cap2;
-  S* agg = (S*)alloc(sizeof(S) * FS * npad, actx);
-  S* aux1 = (S*)alloc(sizeof(S) * FS * (aux1n ? aux1n : 1), actx);
-  S* aux2 = (S*)alloc(sizeof(S) * FS * (aux2n ? aux2n : 1), actx);
-  void* dlb_state = dlb ? alloc(dlb_state_bytes<S, NX>(nchunks), actx) : nullptr;
-  if (!agg || !aux1 || !aux2 || (dlb && !dlb_state)) return 8;
-
-  FastFilterOps<S, NX> fops{L.err};
-  FastSmootherOps<S, NX> sops{L.err};
-  const int g = blocks_for(nchunks, kBlock);
-
-  // ---- forward filter (PKF; first half of PRTS / PTFS) ----
-  k_filter_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nchunks, agg, npad, L.err);
-  L.count("filter_reduce");
-  if (npad > nchunks) {
-    k_fill_identity<<<blocks_for(npad - nchunks, kBlock), kBlock, 0, L.stream>>>(
-        fops, ElemBuf<S>{agg, npad, npad, 0}, nchunks, npad);
-    L.count("fill_identity");
-  }
-  chunk_scan(L, fops, a, agg, nchunks, npad, 0, aux1, aux2, plan, dlb_state);
-  k_filter_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nchunks, agg, npad, mean, cov, L.err);
-  L.count("filter_finish");
-
-  if (a.method == 1) {  // ---- RTS smoother ----
-    k_smoother_reduce<S, NX><<<g, kBlock, 0, L.stream>>>(m, mean, cov, Lc, nchunks, agg, npad, L.err);
-    L.count("smoother_reduce");
-    if (npad > nchunks) {
-      k_fill_identity<<<blocks_for(npad - nchunks, kBlock), kBlock, 0, L.stream>>>(
-          sops, ElemBuf<S>{agg, npad, npad, 0}, nchunks, npad);
-      L.count("fill_identity");
-    }
-    chunk_scan(L, sops, a, agg, nchunks, npad, 1, aux1, aux2, plan, dlb_state);
-    k_smoother_finish<S, NX><<<g, kBlock, 0, L.stream>>>(m, Lc, nchunks, agg, npad, mean, cov, L.err);
-    L.count("smoother_finish");
-  } else if (a.method == 2) {  // ---- two-filter smoother ----
-    k_bwd_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nchunks, agg, npad, L.err);
-    L.count("bwd_reduce");
-    if (npad > nchunks) {
-      k_fill_identity<<<blocks_for(npad - nchunks, kBlock), kBlock, 0, L.stream>>>(
-          fops, ElemBuf<S>{agg, npad, npad, 0}, nchunks, npad);
-      L.count("fill_identity");
-    }
-    chunk_scan(L, fops, a, agg, nchunks, npad, 1, aux1, aux2, plan, dlb_state);
-    k_bwd_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nchunks, agg, npad, mean, cov, L.err);
-    L.count("bwd_finish_tf_combine");
+static int fast_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean,
+                      S* cov, void* (*alloc)(size_t, void*), void* actx) {
+  if (m.t == 0) return 0;
+  FastScratch<S> sc;
+  int st = fast_prepare_t<S, NX>(m, a, sc, alloc, actx);
+  if (st) return st;
+  fast_phase_t<S, NX, NY>(L, m, a, sc, 0, mean, cov, nullptr, nullptr);
+  fast_phase_t<S, NX, NY>(L, m, a, sc, 1, mean, cov, nullptr, nullptr);
+  if (a.method == 1) {
+    fast_phase_t<S, NX, NY>(L, m, a, sc, 2, mean, cov, nullptr, nullptr);
+    fast_phase_t<S, NX, NY>(L, m, a, sc, 3, mean, cov, nullptr, nullptr);
+  } else if (a.method == 2) {
+    fast_phase_t<S, NX, NY>(L, m, a, sc, 4, mean, cov, nullptr, nullptr);
+    fast_phase_t<S, NX, NY>(L, m, a, sc, 5, mean, cov, nullptr, nullptr);
   }
   return 0;
 }
@@ -137,12 +192,58 @@ bool fast_supported(int nx, int ny) {
 }
 
 template <typename S>
-int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
-             S* mean, S* cov, void* (*alloc)(size_t, void*), void* actx) {
+int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
+             void* (*alloc)(size_t, void*), void* actx) {
 #define PSK_CASE(A, B) \
   if (m.nx == A && m.ny == B) return fast_run_t<S, A, B>(L, m, a, mean, cov, alloc, actx);
   PSK_FAST_DIMS(PSK_CASE)
 #undef PSK_CASE
+  return -1;
+}
+
+// one phase of a sharded run; `scratch` is an opaque FastScratch<S> owned by
+// the caller (allocated on phase 0 / 2 with the persistent allocator)
+template <typename S>
+int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
+                     void** scratch, S* mean, S* cov, const S* carry, S* elem_out,
+                     void* (*alloc)(size_t, void*), void* actx) {
+  auto* sc = static_cast<FastScratch<S>*>(*scratch);
+  if (!sc) {
+    sc = new FastScratch<S>();
+    *scratch = sc;
+  }
+#define PSK_CASE(A, B)                                                           \
+  if (m.nx == A && m.ny == B) {                                                  \
+    if (phase == 0 || phase == 2) {                                              \
+      int st = fast_prepare_t<S, A>(m, a, *sc, alloc, actx);                    \
+      if (st) return st;                                                         \
+    }                                                                            \
+    return fast_phase_t<S, A, B>(L, m, a, *sc, phase, mean, cov, carry, elem_out); \
+  }
+  PSK_FAST_DIMS(PSK_CASE)
+#undef PSK_CASE
+  return -1;
+}
+template <typename S>
+void fast_shard_release(void* scratch) {
+  delete static_cast<FastScratch<S>*>(scratch);
+}
+
+// folds of gathered shard elements (one thread; count <= number of ranks)
+template <typename S>
+int fast_fold(ExactLaunch& L, int kind, int nx, const S* aggs, int count, S* out) {
+  if (count <= 0) return 7;
+#define PSK_FOLD(N)                                                            \
+  if (nx == N) {                                                               \
+    if (kind == 0)                                                             \
+      k_fold_filter<S, N><<<1, 32, 0, L.stream>>>(aggs, count, out, L.err);    \
+    else                                                                       \
+      k_fold_smoother<S, N><<<1, 32, 0, L.stream>>>(aggs, count, out);         \
+    L.count(kind == 0 ? "fold_filter" : "fold_smoother");                      \
+    return 0;                                                                  \
+  }
+  PSK_FOLD(1) PSK_FOLD(2) PSK_FOLD(3) PSK_FOLD(4)
+#undef PSK_FOLD
   return -1;
 }
 

@@ -1,0 +1,61 @@
+// psk_peak.cu -- FP64 / FP32 FMA-pipe peak microbenchmark (measurement tool
+// for the roofline denominators that MEASURED_PEAKS.json does not carry; not
+// part of the C-ABI product).  Built into libpsk_tools.so.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_fma(T* out, int iters, T a, T b) {
+  // 8 independent chains per thread keep the FMA pipe full
+  T x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4,
+    x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  T s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == T(-12345)) out[0] = s;  // keep the chains live
+}
+
+template <typename T>
+int run(int device, double* tflops, double* ms_out) {
+  cudaSetDevice(device);
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, device);
+  T* out;
+  cudaMalloc(&out, sizeof(T));
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_fma<T><<<blocks, threads>>>(out, 64, T(0.999999), T(1e-7));  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_fma<T><<<blocks, threads>>>(out, iters, T(0.999999), T(1e-7));
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return 5;
+  const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  *ms_out = best;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int psk_peak_fma(int device, int f64, double* tflops, double* ms) {
+  return f64 ? run<double>(device, tflops, ms) : run<float>(device, tflops, ms);
+}

@@ -1,0 +1,147 @@
+"""Multi-GPU time sharding of the parallel RTS smoother.
+
+One process per GPU.  Rank g owns the contiguous steps [lo, hi) of the series
+(plus one extra transition (F, Q, u) for the smoother boundary).  The only
+data-path exchanges are two tiny all_gathers of shard elements -- one
+filtering element (3 nx^2 + 2 nx scalars) and one smoothing element
+(2 nx^2 + nx) per rank, NCCL over NVLink on the GPU box:
+
+  1. filter reduce+scan on the shard        -> shard element a_g
+  2. all_gather(a_0 .. a_{G-1})
+  3. carry_g = a_0 (x) ... (x) a_{g-1}       (non-commutative, rank order; a_0
+                                              contains a_1 with A = 0, so the
+                                              fold is the filtered state at lo-1)
+  4. filter finish from carry_g             -> filtered stats of the shard
+  5. smoother reduce+scan                   -> shard suffix element s_g
+  6. all_gather(s_0 .. s_{G-1})
+  7. carry'_g = s_{g+1} (x) ... (x) s_{G-1}  (s_{G-1} contains a_T with E = 0:
+                                              the smoothed state at hi)
+  8. smoother finish from carry'_g          -> smoothed stats of the shard
+
+The fix-up is not a separate pass: the carried state enters the finish
+kernels that write the outputs anyway.  `prts_run_sharded` is written against
+a small engine interface so that the same orchestration runs on the CUDA
+engine (product) and, in the CPU tests, on an oracle-backed engine over gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Any
+
+from . import _lib
+
+
+def shard_range(t: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous near-equal split of [0, t) (earlier ranks get the remainder)."""
+    base, rem = divmod(t, world)
+    lo = rank * base + min(rank, rem)
+    hi = lo + base + (1 if rank < rem else 0)
+    return lo, hi
+
+
+class CudaShardEngine:
+    """Shard phases on one GPU through the C-ABI (psk_shard_*, psk_fold_*)."""
+
+    def __init__(self, be, model, ys, flags: int, t_shard: int):
+        from .api import _Marshal
+        self.be = be
+        self.mk = _Marshal(model, ys)
+        if self.mk.device is None:
+            raise ValueError("sharded runs take CUDA tensors")
+        self.mk.model.t = t_shard  # f/u/q may hold one extra transition
+        self.mk.t = t_shard
+        self.flags = flags
+        self.nx = self.mk.nx
+        import torch
+        self.torch = torch
+        self.dt = torch.float64 if self.mk.f64 else torch.float32
+        self.dev = self.mk.device
+
+    def _p(self, t):
+        return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+    def empty(self, n):
+        return self.torch.empty(n, dtype=self.dt, device=self.dev)
+
+    def filter_reduce(self, spec):
+        from .api import _check
+        out = self.empty(3 * self.nx * self.nx + 2 * self.nx)
+        _check(_lib.lib().psk_shard_filter_reduce(self.be.handle, C.byref(self.mk.model),
+                                                  self.flags, int(spec.alg),
+                                                  int(spec.sengupta_n), self._p(out)))
+        return out
+
+    def filter_finish(self, carry, mean, cov):
+        from .api import _check
+        _check(_lib.lib().psk_shard_filter_finish(self.be.handle, C.byref(self.mk.model),
+                                                  self.flags, self._p(carry), self._p(mean),
+                                                  self._p(cov)))
+
+    def smoother_reduce(self, spec, mean, cov):
+        from .api import _check
+        out = self.empty(2 * self.nx * self.nx + self.nx)
+        _check(_lib.lib().psk_shard_smoother_reduce(self.be.handle, C.byref(self.mk.model),
+                                                    self.flags, int(spec.alg),
+                                                    int(spec.sengupta_n), self._p(mean),
+                                                    self._p(cov), self._p(out)))
+        return out
+
+    def smoother_finish(self, carry, mean, cov):
+        from .api import _check
+        _check(_lib.lib().psk_shard_smoother_finish(self.be.handle, C.byref(self.mk.model),
+                                                    self.flags, self._p(carry), self._p(mean),
+                                                    self._p(cov)))
+
+    def fold(self, kind: str, elems):
+        from .api import _check
+        st = self.empty(self.nx + self.nx * self.nx)
+        stacked = self.torch.stack(list(elems)).contiguous()
+        fn = _lib.lib().psk_fold_filter if kind == "filter" else _lib.lib().psk_fold_smoother
+        _check(fn(self.be.handle, _lib.PSK_F64 if self.mk.f64 else _lib.PSK_F32, self.nx,
+                  self._p(stacked), len(elems), self._p(st)))
+        return st
+
+    def stats(self, t):
+        return (self.torch.empty((t, self.nx), dtype=self.dt, device=self.dev),
+                self.torch.empty((t, self.nx, self.nx), dtype=self.dt, device=self.dev))
+
+
+def all_gather(x, world: int, group: Any = None):
+    import torch.distributed as dist
+    out = [x.new_empty(x.shape) for _ in range(world)]
+    dist.all_gather(out, x, group=group)
+    return out
+
+
+def prts_sharded(engine, spec, rank: int, world: int, t_shard: int, group: Any = None):
+    """Steps 1-8 above on one rank; returns the shard's smoothed (mean, cov)."""
+    a = engine.filter_reduce(spec)
+    gathered = all_gather(a, world, group) if world > 1 else [a]
+    carry = engine.fold("filter", gathered[:rank]) if rank > 0 else None
+    mean, cov = engine.stats(t_shard)
+    engine.filter_finish(carry, mean, cov)
+    s = engine.smoother_reduce(spec, mean, cov)
+    gathered = all_gather(s, world, group) if world > 1 else [s]
+    carry = engine.fold("smoother", gathered[rank + 1:]) if rank < world - 1 else None
+    engine.smoother_finish(carry, mean, cov)
+    return mean, cov
+
+
+def shard_flags(rank: int, world: int) -> int:
+    return (_lib.PSK_SHARD_FIRST if rank == 0 else 0) | \
+        (_lib.PSK_SHARD_LAST if rank == world - 1 else 0)
+
+
+def prts_run_sharded(model, ys, spec, be, rank: int, world: int, lo: int, hi: int,
+                     t_total: int, group: Any = None, engine: Any = None):
+    """PRTS over the shard [lo, hi) of a T-step series.  `model`/`ys` hold the
+    shard's steps (f/u/q with one extra transition unless hi == T).  world == 1
+    is the plain single-GPU prts_run."""
+    from . import api
+
+    if world == 1:
+        return api.prts_run(model, ys, spec, be)
+    if engine is None:
+        engine = CudaShardEngine(be, model, ys, shard_flags(rank, world), hi - lo)
+    mean, cov = prts_sharded(engine, spec, rank, world, hi - lo, group)
+    return api.GaussianStats(mean, cov)

@@ -231,9 +231,12 @@ def test_empty_and_contracts(psk, fast, exact):
 
 
 def test_not_positive_definite(psk, fast, exact, port):
+    from oracle.oracle import OracleError
     m, ys = gen(port, 1, 4, 2, 50)
     m.r = m.r.copy()
-    m.r[10] = -np.eye(2)
+    m.r[10] = -1e3 * np.eye(2)  # S = H Q H^T + R is indefinite at step 11
+    with pytest.raises(OracleError):
+        port.pkf_run(m, ys, 3)
     for be in (fast, exact):
         with pytest.raises(psk.NotPositiveDefinite):
             psk.pkf_run(m, ys, psk.ScanSpec(psk.ScanAlg.InplaceLaFi), be)

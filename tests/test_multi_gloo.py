@@ -1,0 +1,152 @@
+"""The N>1 time-sharded PRTS orchestration (distributed.py) on CPU ranks over
+gloo: the same prts_sharded() the GPU ranks run, driven by an oracle-backed
+shard engine, must reproduce the sequential RTS smoother of the whole series
+for world sizes 2 and 3 (uneven shards).  Checks the exchange order, the
+non-commutative prefix / suffix folds and the shard-boundary handling (extra
+transition, prior only on rank 0, a_T only on the last rank)."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+class OracleShardEngine:
+    """Reference-algorithm shard phases on the CPU (tests only)."""
+
+    def __init__(self, orc, m, ys, lo, hi):
+        import torch
+        self.o, self.m, self.ys, self.lo, self.hi = orc, m, ys, lo, hi
+        self.nx = m.nx
+        self.torch = torch
+
+    def _t(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a))
+
+    def filter_reduce(self, spec):
+        acc = None
+        for k in range(self.lo + 1, self.hi + 1):  # 1-based steps of the shard
+            e = self.o.make_filter_element(self.m, self.ys, k)
+            acc = e if acc is None else self.o.filter_combine(self.nx, acc, e)
+        return self._t(acc)
+
+    def fold(self, kind, elems):
+        els = [np.asarray(e) for e in elems]
+        nx = self.nx
+        if kind == "filter":
+            acc = els[0]
+            for e in els[1:]:
+                acc = self.o.filter_combine(nx, acc, e)
+            b, c = acc[nx * nx:nx * nx + nx], acc[nx * nx + nx:2 * nx * nx + nx]
+        else:
+            acc = els[-1]
+            for e in els[-2::-1]:
+                acc = self.o.smoother_combine(nx, e, acc)
+            b, c = acc[nx * nx:nx * nx + nx], acc[nx * nx + nx:]
+        return self._t(np.concatenate([b, c]))
+
+    def stats(self, t):
+        return np.zeros((t, self.nx)), np.zeros((t, self.nx, self.nx))
+
+    def _slice(self, prior=None):
+        from paper_2511_10363_b200.api import Lgssm
+        s = slice(self.lo, self.hi)
+        m = self.m
+        pm, pc = (m.prior_mean, m.prior_cov) if prior is None else prior
+        return Lgssm(f=m.f[s], u=m.u[s], q=m.q[s], h=m.h[s], d=m.d[s], r=m.r[s],
+                     prior_mean=pm, prior_cov=pc, t=self.hi - self.lo), self.ys[s]
+
+    def filter_finish(self, carry, mean, cov):
+        nx = self.nx
+        prior = None
+        if carry is not None:
+            c = np.asarray(carry)
+            prior = (c[:nx].copy(), c[nx:].reshape(nx, nx).copy())
+        sm, sys_ = self._slice(prior)
+        fm, fc = self.o.kf_run(sm, sys_)
+        mean[:], cov[:] = fm, fc
+
+    def smoother_reduce(self, spec, mean, cov):
+        acc = None
+        for i in range(self.hi - 1, self.lo - 1, -1):
+            e = self.o.make_smoother_element(self.m, self.ys, mean[i - self.lo],
+                                             cov[i - self.lo], i + 1)
+            acc = e if acc is None else self.o.smoother_combine(self.nx, e, acc)
+        return self._t(acc)
+
+    def smoother_finish(self, carry, mean, cov):
+        nx = self.nx
+        state = None
+        if carry is not None:
+            c = np.asarray(carry)
+            state = np.concatenate([np.zeros(nx * nx), c])  # (E=0, g, L)
+        for i in range(self.hi - 1, self.lo - 1, -1):
+            e = self.o.make_smoother_element(self.m, self.ys, mean[i - self.lo],
+                                             cov[i - self.lo], i + 1)
+            state = e if state is None else self.o.smoother_combine(nx, e, state)
+            mean[i - self.lo] = state[nx * nx:nx * nx + nx]
+            cov[i - self.lo] = state[nx * nx + nx:].reshape(nx, nx)
+
+
+def _worker(rank, world, port, t, out_dir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+
+    from conftest import gen
+    from oracle.oracle import Oracle
+    from paper_2511_10363_b200.api import ScanSpec
+    from paper_2511_10363_b200.distributed import prts_sharded, shard_range
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle("port")
+    m, ys = gen(orc, 12, 4, 2, t)
+    lo, hi = shard_range(t, rank, world)
+    eng = OracleShardEngine(orc, m, ys, lo, hi)
+    mean, cov = prts_sharded(eng, ScanSpec(), rank, world, hi - lo)
+    np.savez(Path(out_dir) / f"r{rank}.npz", mean=mean, cov=cov, lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,t", [(2, 101), (3, 64)])
+def test_sharded_prts_matches_sequential(tmp_path, port, world, t):
+    import torch.multiprocessing as mp
+
+    from conftest import gen, max_rel_err
+    mp.spawn(_worker, args=(world, _free_port(), t, str(tmp_path)), nprocs=world, join=True)
+    m, ys = gen(port, 12, 4, 2, t)
+    rm, rc = port.rts_run(m, ys)
+    covered = 0
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        lo, hi = int(d["lo"]), int(d["hi"])
+        assert lo == covered
+        covered = hi
+        assert max_rel_err(d["mean"], d["cov"], rm[lo:hi], rc[lo:hi]) < 1e-9, r
+    assert covered == t
+
+
+def test_shard_range_partition():
+    from paper_2511_10363_b200.distributed import shard_range
+    for t in (1, 7, 64, 1000):
+        for w in (1, 2, 3, 8):
+            spans = [shard_range(t, r, w) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == t
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
