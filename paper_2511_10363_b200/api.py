@@ -158,8 +158,8 @@ class CudaBackend:
     reference's ``PoolBackend`` it must not be driven by two callers at once.
     """
 
-    def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 32,
-                 stream: Any = None) -> None:
+    def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 64,
+                 stream: Any = None, prefetch: int | None = None) -> None:
         L = _lib.lib()
         ctx = C.c_void_p()
         _check(L.psk_create(C.byref(ctx), int(device)))
@@ -167,8 +167,13 @@ class CudaBackend:
         self.device = int(device)
         self.set_mode(mode)
         self.set_chunk(chunk)
+        if prefetch is not None:
+            self.set_option("prefetch", prefetch)
         if stream is not None:
             self.set_stream(stream)
+
+    def set_option(self, key: str, value: int) -> None:
+        _check(_lib.lib().psk_set_option(self._ctx, key.encode(), int(value)))
 
     # reference Backend interface: host closures cannot run on the device
     def run(self, launch: Any) -> None:  # backend.hpp:42

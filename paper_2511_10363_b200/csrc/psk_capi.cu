@@ -36,7 +36,8 @@ struct psk_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int mode = PSK_MODE_FAST;
-  long long chunk = 32;
+  long long chunk = 64;
+  int prefetch = 1;
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
@@ -44,6 +45,8 @@ struct psk_ctx {
   std::vector<void*> persist;  // sharded-run scratch kept between calls
   void* shard_scratch = nullptr;
   int shard_dtype = -1;
+  int shard_alg = 6;
+  uint64_t shard_sn = 1;
   std::vector<std::pair<const char*, float>> profile;
 };
 
@@ -218,6 +221,7 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     a.alg = alg;
     a.sengupta_n = sengupta_n;
     a.chunk = ctx->chunk;
+    a.prefetch = ctx->prefetch;
     st = fast_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
     if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
     if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
@@ -303,7 +307,15 @@ int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   a.alg = alg;
   a.sengupta_n = sn;
   a.chunk = ctx->chunk;
-  if (phase == 0 || phase == 2) {
+  a.prefetch = ctx->prefetch;
+  if (phase != 0 && phase != 2) {  // finishes reuse the scan spec of the reduce
+    a.alg = ctx->shard_alg;
+    a.sengupta_n = ctx->shard_sn;
+  } else {
+    ctx->shard_alg = alg;
+    ctx->shard_sn = sn;
+  }
+  if (phase == 0) {
     ctx_free_persist(ctx);
     if (ctx->shard_scratch) {
       if (ctx->shard_dtype == PSK_F64) fast_shard_release<double>(ctx->shard_scratch);
@@ -461,6 +473,21 @@ int psk_set_chunk(psk_ctx* c, int chunk) {
   if (!c) return fail(PSK_E_ARG, "null context");
   if (chunk < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
   c->chunk = chunk;
+  return PSK_OK;
+}
+
+int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return fail(PSK_E_ARG, "null context or key");
+  const std::string k(key);
+  if (k == "chunk") {
+    if (value < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
+    c->chunk = value;
+  } else if (k == "prefetch") {
+    if (value < 0 || value > 2) return fail(PSK_E_ARG, "prefetch must be 0, 1 or 2");
+    c->prefetch = (int)value;
+  } else {
+    return fail(PSK_E_ARG, "unknown option " + k);
+  }
   return PSK_OK;
 }
 

@@ -19,6 +19,7 @@
 #pragma once
 #include "psk_common.cuh"
 #include "psk_mat.cuh"
+#include "psk_stage.cuh"
 
 namespace psk {
 
@@ -391,14 +392,94 @@ __device__ __forceinline__ void filter_apply(Vec<S, NX>& x, Mat<S, NX, NX>& P,
 }
 
 // ============================================================================
-// Filter kernels
+// Staged per-step kernels.  Each thread owns one chunk of consecutive steps;
+// the per-step model blocks of step k+1 (k-1 when walking backwards) are
+// fetched into shared memory with cp.async while step k is computed.
+// Blocks are one warp (NT = 32) so that ~8 CTAs of 226-register threads fit
+// per SM together with their 2 x 13 KB stages.
 // ============================================================================
+constexpr int kStageNT = 128;
+
+__device__ __forceinline__ void prefetch_line(const void* p, int pf) {
+  if (pf == 1)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  else if (pf == 2)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Step view: per-step model blocks read straight from global memory (each
+// block is one thread's contiguous 16..128 B; L1 serves the rest of a line).
+template <typename S>
+struct FStep {
+  const ModelView<S>* m;
+  long long k;
+};
+
+// prefetch the lines of step k's model blocks (pf: 0 off, 1 L1, 2 L2)
+template <typename S, int NX, int NY>
+__device__ __forceinline__ void prefetch_filter_in(const ModelView<S>& m, long long k, int pf) {
+  if (pf == 0) return;
+  prefetch_line(m.F(k), pf);
+  prefetch_line(m.Q(k), pf);
+  prefetch_line(m.U(k), pf);
+  prefetch_line(m.H(k), pf);
+  prefetch_line(m.D(k), pf);
+  prefetch_line(m.R(k), pf);
+  prefetch_line(m.Y(k), pf);
+}
+// predict with (F, u, Q)_k + update with y_k
+template <typename S, int NX, int NY>
+__device__ __forceinline__ void kf_step(Vec<S, NX>& x, Mat<S, NX, NX>& P,
+                                        const ModelView<S>& m, long long k, unsigned& err) {
+  kf_predict(x, P, m, k);
+  kf_update(x, P, load_meas<S, NX, NY>(m, k), err);
+}
+
+// Smoothing element of step i from the filtered (x, P)_i and the transition
+// (F, Q, u)_{i+1} passed in registers (kalman_elems.hpp:151-193).
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> smoother_elem(const Vec<S, NX>& x,
+                                                      const Mat<S, NX, NX>& P,
+                                                      const Mat<S, NX, NX>& F,
+                                                      const Mat<S, NX, NX>& Q,
+                                                      const Vec<S, NX>& u, unsigned& err) {
+  SElem<S, NX> e;
+  const Mat<S, NX, NX> fp = mul(F, P);
+  const Mat<S, NX, NX> pp = mul_nt_sym_add(fp, F, Q);
+  const Chol<S, NX> ch = cholesky(pp, err);
+  const Mat<S, NX, NX> et = chol_solve(ch, fp);  // E^T
+  e.E = trans(et);
+  const Vec<S, NX> fx = mul_add(F, x, u);
+  e.g = sub_mul(x, e.E, fx);
+  Mat<S, NX, NX> o;
+#pragma unroll
+  for (int a = 0; a < NX; ++a)
+#pragma unroll
+    for (int b = a; b < NX; ++b) {
+      S acc = P.a[a][b];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) acc = sfma(-et.a[k][a], fp.a[k][b], acc);
+      o.a[a][b] = acc;
+      o.a[b][a] = acc;
+    }
+  e.L = o;
+  return e;
+}
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> terminal_elem(const Vec<S, NX>& x,
+                                                      const Mat<S, NX, NX>& P) {
+  SElem<S, NX> e;  // a_T = (0, x_T, P_T), kalman_elems.hpp:158-163
+  e.E = zeros<S, NX, NX>();
+  e.g = x;
+  e.L = P;
+  return e;
+}
 
 // reduce: chunk c = steps [c L, min(c L + L, T)) -> one filtering element
 template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kStageNT)
     k_filter_reduce(ModelView<S> m, long long L, long long nchunks, S* agg,
-                    long long cap, unsigned* err) {
+                    long long cap, int pf, unsigned* err) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   unsigned e = 0;
@@ -410,9 +491,9 @@ __global__ void __launch_bounds__(128)
     // is the filtered state itself, so run the chunk in state form.
     Vec<S, NX> x = load<S, NX, 1>(m.m0);
     Mat<S, NX, NX> P = load<S, NX, NX>(m.p0);
-    for (long long k = 0; k < k1; ++k) {
-      kf_predict(x, P, m, k);
-      kf_update(x, P, load_meas<S, NX, NY>(m, k), e);
+    for (long long k = k0; k < k1; ++k) {
+      if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
+      kf_step<S, NX, NY>(x, P, m, k, e);
     }
     a.A = zeros<S, NX, NX>();
     a.b = x;
@@ -422,14 +503,13 @@ __global__ void __launch_bounds__(128)
   } else {
     a = make_filter_elem<S, NX, NY>(m, k0, e);
     for (long long k = k0 + 1; k < k1; ++k) {
-      // predict the conditional: (F A, F b + u, F C F^T + Q)
+      if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
+      // predict the conditional: (F A, F b + u, F C F^T + Q), then update
       const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
-      const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
-      const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
       a.A = mul(F, a.A);
-      a.b = mul_add(F, a.b, u);
+      a.b = mul_add(F, a.b, load<S, NX, 1>(m.U(k)));
       const Mat<S, NX, NX> fc = mul(F, a.C);
-      a.C = mul_nt_sym_add(fc, F, Q);
+      a.C = mul_nt_sym_add(fc, F, load<S, NX, NX>(m.Q(k)));
       cond_update(a, load_meas<S, NX, NY>(m, k), e);
     }
   }
@@ -437,24 +517,15 @@ __global__ void __launch_bounds__(128)
   if (e) atomicOr(err, e);
 }
 
-// finish: sequential Kalman filter over the chunk from the carried prefix
-// (inclusive prefix of chunk c-1 = filtered state at step c L - 1).  In a
-// time-sharded run `carry` holds the filtered state at the step before the
-// shard (the fold of the predecessor shards' elements): the incoming state of
-// chunk c > 0 is then carry (x) (local prefix of chunk c-1), the reduced
-// Lemma-1 combine of a state (A = 0) with an element.
-template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(128)
-    k_filter_finish(ModelView<S> m, long long L, long long nchunks,
-                    const S* pre, long long pre_cap, const S* carry, S* mean,
-                    S* cov, unsigned* err) {
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  unsigned e = 0;
-  const long long k0 = c * L;
-  const long long k1 = min(k0 + L, m.t);
-  Vec<S, NX> x;
-  Mat<S, NX, NX> P;
+// Incoming filtered state of chunk c: the inclusive prefix of chunk c-1 (or
+// the prior).  In a time-sharded run `carry` holds the filtered state before
+// the shard and the incoming state of chunk c > 0 is carry (x) prefix(c-1),
+// the reduced Lemma-1 combine of a state (A = 0) with an element.
+template <typename S, int NX>
+__device__ __forceinline__ void filter_incoming(const ModelView<S>& m, long long c,
+                                                const S* pre, long long pre_cap,
+                                                const S* carry, Vec<S, NX>& x,
+                                                Mat<S, NX, NX>& P, unsigned& e) {
   if (c == 0) {
     if (m.prior_first) {
       x = load<S, NX, 1>(m.m0);
@@ -471,10 +542,51 @@ __global__ void __launch_bounds__(128)
     P = load<S, NX, NX>(carry + NX);
     filter_apply(x, P, fe_load<S, NX>(pre, pre_cap, c - 1), e);
   }
+}
+
+// finish: sequential Kalman filter over the chunk from the carried prefix.
+// With `sagg` non-null (PRTS) the same pass also folds the chunk's smoothing
+// element e_{k0} (x) ... (x) e_{k1-1} (Lemma 2 is associative, so the chunk
+// element is built forwards): e_{k-1} needs the filtered state of step k-1
+// and the transition (F, Q, u)_k that the filter loads for step k anyway.
+template <typename S, int NX, int NY>
+__global__ void __launch_bounds__(kStageNT)
+    k_filter_finish(ModelView<S> m, long long L, long long nchunks, const S* pre,
+                    long long pre_cap, const S* carry, S* mean, S* cov, S* sagg,
+                    long long scap, int pf, unsigned* err) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  unsigned e = 0;
+  const long long k0 = c * L;
+  const long long k1 = min(k0 + L, m.t);
+  Vec<S, NX> x;
+  Mat<S, NX, NX> P;
+  filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
+  SElem<S, NX> sa;
   for (long long k = k0; k < k1; ++k) {
-    kf_predict(x, P, m, k);
+    if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
+    const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
+    const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
+    const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
+    if (sagg != nullptr && k > k0) {  // (x, P) still hold the filtered step k-1
+      const SElem<S, NX> ek = smoother_elem(x, P, F, Q, u, e);
+      sa = k - 1 == k0 ? ek : smoother_combine(sa, ek);
+    }
+    x = mul_add(F, x, u);
+    const Mat<S, NX, NX> fp = mul(F, P);
+    P = mul_nt_sym_add(fp, F, Q);
     kf_update(x, P, load_meas<S, NX, NY>(m, k), e);
     store_state(mean, cov, k, x, P);
+  }
+  if (sagg != nullptr) {  // element of the chunk's last step
+    SElem<S, NX> ek;
+    if (k1 - 1 == m.last_step)
+      ek = terminal_elem(x, P);
+    else
+      ek = smoother_elem(x, P, load<S, NX, NX>(m.F(k1)), load<S, NX, NX>(m.Q(k1)),
+                         load<S, NX, 1>(m.U(k1)), e);
+    sa = k1 - 1 == k0 ? ek : smoother_combine(sa, ek);
+    se_store(sagg, scap, c, sa);
   }
   if (e) atomicOr(err, e);
 }
@@ -483,25 +595,48 @@ __global__ void __launch_bounds__(128)
 // RTS smoother kernels (reverse direction)
 // ============================================================================
 
-// reduce: suffix element a_{k0} (x) ... (x) a_{k1-1} of the chunk
 template <typename S, int NX>
-__global__ void __launch_bounds__(128)
-    k_smoother_reduce(ModelView<S> m, const S* fmean, const S* fcov,
-                      long long L, long long nchunks, S* agg, long long cap,
-                      unsigned* err) {
+__device__ __forceinline__ void prefetch_smoother_in(const ModelView<S>& m, const S* mean,
+                                                     const S* cov, long long i, int pf) {
+  if (pf == 0) return;
+  prefetch_line(mean + i * NX, pf);
+  prefetch_line(cov + i * NX * NX, pf);
+  if (i != m.last_step) {
+    prefetch_line(m.F(i + 1), pf);
+    prefetch_line(m.Q(i + 1), pf);
+    prefetch_line(m.U(i + 1), pf);
+  }
+}
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> smoother_elem_at(const ModelView<S>& m, long long i,
+                                                         const Vec<S, NX>& x,
+                                                         const Mat<S, NX, NX>& P,
+                                                         unsigned& e) {
+  if (i == m.last_step) return terminal_elem(x, P);
+  return smoother_elem(x, P, load<S, NX, NX>(m.F(i + 1)), load<S, NX, NX>(m.Q(i + 1)),
+                       load<S, NX, 1>(m.U(i + 1)), e);
+}
+
+// reduce (used when the filter finish did not build the smoother chunk
+// elements, e.g. a sharded smoother-reduce call): suffix element
+// a_{k0} (x) ... (x) a_{k1-1} of the chunk, built backwards
+template <typename S, int NX>
+__global__ void __launch_bounds__(kStageNT)
+    k_smoother_reduce(ModelView<S> m, const S* fmean, const S* fcov, long long L,
+                      long long nchunks, S* agg, long long cap, int pf, unsigned* err) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   unsigned e = 0;
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, m.t);
-  Vec<S, NX> x;
-  Mat<S, NX, NX> P;
-  load_state(fmean, fcov, k1 - 1, x, P);
-  SElem<S, NX> a = make_smoother_elem(m, k1 - 1, x, P, e);
-  for (long long i = k1 - 2; i >= k0; --i) {
+  SElem<S, NX> a;
+  for (long long i = k1 - 1; i >= k0; --i) {
+    if (i > k0) prefetch_smoother_in<S, NX>(m, fmean, fcov, i - 1, pf);
+    Vec<S, NX> x;
+    Mat<S, NX, NX> P;
     load_state(fmean, fcov, i, x, P);
-    const SElem<S, NX> ei = make_smoother_elem(m, i, x, P, e);
-    a = smoother_combine(ei, a);
+    const SElem<S, NX> ei = smoother_elem_at<S, NX>(m, i, x, P, e);
+    a = i == k1 - 1 ? ei : smoother_combine(ei, a);
   }
   se_store(agg, cap, c, a);
   if (e) atomicOr(err, e);
@@ -509,14 +644,14 @@ __global__ void __launch_bounds__(128)
 
 // finish: sequential RTS over the chunk from the carried suffix (the
 // inclusive reversed prefix of chunk c+1 = smoothed state at step k1).  In a
-// time-sharded run `carry` holds the smoothed state at the step after the
-// shard (fold of the successor shards' elements, E = 0): the incoming state of
-// chunk c < nchunks-1 is (local suffix of chunk c+1) (x) carry.
+// time-sharded run `carry` holds the smoothed state after the shard (fold of
+// the successor shards' elements, E = 0): the incoming state of chunk
+// c < nchunks-1 is then (local suffix of chunk c+1) (x) carry.
 template <typename S, int NX>
-__global__ void __launch_bounds__(128)
-    k_smoother_finish(ModelView<S> m, long long L, long long nchunks,
-                      const S* suf, long long suf_cap, const S* carry, S* mean,
-                      S* cov, unsigned* err) {
+__global__ void __launch_bounds__(kStageNT)
+    k_smoother_finish(ModelView<S> m, long long L, long long nchunks, const S* suf,
+                      long long suf_cap, const S* carry, S* mean, S* cov, int pf,
+                      unsigned* err) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   unsigned e = 0;
@@ -541,8 +676,9 @@ __global__ void __launch_bounds__(128)
     Ls = load<S, NX, NX>(carry + NX);
   }
   // `mean`/`cov` hold the filtered stats on entry (in place: each step is
-  // read before it is overwritten by the same thread)
+  // read before the same thread overwrites it)
   for (long long i = k1 - 1; i >= k0; --i) {
+    if (i > k0) prefetch_smoother_in<S, NX>(m, mean, cov, i - 1, pf);
     Vec<S, NX> x;
     Mat<S, NX, NX> P;
     load_state(mean, cov, i, x, P);
@@ -550,7 +686,7 @@ __global__ void __launch_bounds__(128)
       gs = x;
       Ls = P;
     } else {
-      const SElem<S, NX> ei = make_smoother_elem(m, i, x, P, e);
+      const SElem<S, NX> ei = smoother_elem_at<S, NX>(m, i, x, P, e);
       gs = mul_add(ei.E, gs, ei.g);
       const Mat<S, NX, NX> el = mul(ei.E, Ls);
       Ls = mul_nt_sym_add(el, ei.E, ei.L);

@@ -54,6 +54,8 @@ struct FastScratch {
   long long nchunks = 0, npad = 0, chunk = 1;
   ScanPlan plan;
   S *agg = nullptr, *aux1 = nullptr, *aux2 = nullptr;
+  S* sagg = nullptr;        // smoother chunk elements (built by the filter finish)
+  bool sagg_valid = false;
   void* dlb = nullptr;
 };
 
@@ -72,10 +74,12 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
   constexpr int FS = FLayout<NX>::size;
   const long long a1 = dlb ? 0 : sc.plan.cap1, a2 = dlb ? 0 : sc.plan.cap2;
   sc.agg = (S*)alloc(sizeof(S) * FS * (sc.npad ? sc.npad : 1), actx);
+  sc.sagg = (S*)alloc(sizeof(S) * SLayout<NX>::size * (sc.npad ? sc.npad : 1), actx);
+  sc.sagg_valid = false;
   sc.aux1 = (S*)alloc(sizeof(S) * FS * (a1 ? a1 : 1), actx);
   sc.aux2 = (S*)alloc(sizeof(S) * FS * (a2 ? a2 : 1), actx);
   sc.dlb = dlb ? alloc(dlb_state_bytes<S, NX>(sc.nchunks), actx) : nullptr;
-  if (!sc.agg || !sc.aux1 || !sc.aux2 || (dlb && !sc.dlb)) return 8;
+  if (!sc.agg || !sc.sagg || !sc.aux1 || !sc.aux2 || (dlb && !sc.dlb)) return 8;
   return 0;
 }
 
@@ -94,49 +98,57 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
   FastFilterOps<S, NX> fops{L.err};
   FastSmootherOps<S, NX> sops{L.err};
   const int g = blocks_for(nch, kBlock);
-  auto fill = [&](auto ops) {
+  auto fill = [&](auto ops, S* buf) {
     if (npad > nch) {
       k_fill_identity<<<blocks_for(npad - nch, kBlock), kBlock, 0, L.stream>>>(
-          ops, ElemBuf<S>{sc.agg, npad, npad, 0}, nch, npad);
+          ops, ElemBuf<S>{buf, npad, npad, 0}, nch, npad);
       L.count("fill_identity");
     }
   };
+  const int gs = blocks_for(nch, kStageNT);
+  const int pf = a.prefetch;
   switch (phase) {
     case 0:
-      k_filter_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, L.err);
+      k_filter_reduce<S, NX, NY><<<gs, kStageNT, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, pf,
+                                                                L.err);
       L.count("filter_reduce");
-      fill(fops);
+      fill(fops, sc.agg);
       chunk_scan(L, fops, a, sc.agg, nch, npad, 0, sc.aux1, sc.aux2, sc.plan, sc.dlb);
       if (elem_out) {
         k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, npad, nch - 1, FLayout<NX>::size, elem_out);
         L.count("extract_elem");
       }
       break;
-    case 1:
-      k_filter_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, carry,
-                                                             mean, cov, L.err);
-      L.count("filter_finish");
+    case 1:  // filter finish; for PRTS also folds the smoother chunk elements
+      k_filter_finish<S, NX, NY><<<gs, kStageNT, 0, L.stream>>>(
+          m, Lc, nch, sc.agg, npad, carry, mean, cov, a.method == 1 ? sc.sagg : nullptr, npad,
+          pf, L.err);
+      L.count(a.method == 1 ? "filter_finish_smoother_reduce" : "filter_finish");
+      sc.sagg_valid = a.method == 1;
       break;
     case 2:
-      k_smoother_reduce<S, NX><<<g, kBlock, 0, L.stream>>>(m, mean, cov, Lc, nch, sc.agg, npad,
-                                                           L.err);
-      L.count("smoother_reduce");
-      fill(sops);
-      chunk_scan(L, sops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      if (!sc.sagg_valid) {
+        k_smoother_reduce<S, NX><<<gs, kStageNT, 0, L.stream>>>(m, mean, cov, Lc, nch,
+                                                                sc.sagg, npad, pf, L.err);
+        L.count("smoother_reduce");
+      }
+      fill(sops, sc.sagg);
+      chunk_scan(L, sops, a, sc.sagg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
       if (elem_out) {
-        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, npad, 0, SLayout<NX>::size, elem_out);
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.sagg, npad, 0, SLayout<NX>::size, elem_out);
         L.count("extract_elem");
       }
       break;
     case 3:
-      k_smoother_finish<S, NX><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, carry,
-                                                           mean, cov, L.err);
+      k_smoother_finish<S, NX><<<gs, kStageNT, 0, L.stream>>>(m, Lc, nch, sc.sagg, npad,
+                                                              carry, mean, cov, pf, L.err);
       L.count("smoother_finish");
+      sc.sagg_valid = false;
       break;
     case 4:
       k_bwd_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, L.err);
       L.count("bwd_reduce");
-      fill(fops);
+      fill(fops, sc.agg);
       chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
       break;
     case 5:
@@ -214,7 +226,7 @@ int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, i
   }
 #define PSK_CASE(A, B)                                                           \
   if (m.nx == A && m.ny == B) {                                                  \
-    if (phase == 0 || phase == 2) {                                              \
+    if (phase == 0) {                                                            \
       int st = fast_prepare_t<S, A>(m, a, *sc, alloc, actx);                    \
       if (st) return st;                                                         \
     }                                                                            \

@@ -260,7 +260,7 @@ def test_launch_count_and_profile(psk, gpu, port):
     prof = be.last_profile()
     names = [n for n, _ in prof]
     assert be.last_launch_count() == len(prof) > 0
-    for k in ("filter_reduce", "chunk_scan_dlb", "filter_finish", "smoother_reduce",
+    for k in ("filter_reduce", "chunk_scan_dlb", "filter_finish_smoother_reduce",
               "smoother_finish"):
         assert k in names
 
