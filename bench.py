@@ -105,15 +105,15 @@ class ClockSampler:
                 "samples": len(self.sm), "source": "nvml"}
 
 
-# algorithmic HBM bytes per time step for each fast-path kernel (nx=4, ny=2;
-# DESIGN.md section 4): inputs 52 scalars, filtered/smoothed stats 20 scalars,
-# smoother inputs (filtered 20 + F,Q,u of the next step 36)
+# algorithmic HBM bytes per time step for each fast-path kernel of PRTS
+# (DESIGN.md section 4): model inputs 52 scalars (nx=4, ny=2), per-step
+# smoothing elements (E, g, upper L) 30 scalars, smoothed stats 20 scalars
 def kernel_bytes_per_step(nx: int, ny: int, s: int) -> dict:
     inp = nx * nx * 2 + nx + ny * nx + ny + ny * ny + ny
     st = nx + nx * nx
-    sm_in = st + 2 * nx * nx + nx
-    return {"filter_reduce": inp * s, "filter_finish": (inp + st) * s,
-            "smoother_reduce": sm_in * s, "smoother_finish": (sm_in + st) * s}
+    egl = nx * nx + nx + nx * (nx + 1) // 2
+    return {"filter_reduce": inp * s, "filter_finish_smoother_reduce": (inp + egl) * s,
+            "smoother_finish": (egl + st) * s}
 
 
 def cpu_reference(T_sample: int, threads: int, runs: int, seed: int = 0) -> dict:
@@ -171,7 +171,7 @@ METRIC = "time-steps/sec filter+smoother (PRTS) vs T, % of HBM roofline"
 def config(args, note: str | None = None) -> dict:
     c = {"workload": f"PRTS T=2^{args.log2t} nx=4 ny=2 damped constant-velocity tracking "
                      f"(BASELINE configs[3] at N={args.gpus})",
-         "T": 1 << args.log2t, "nx": 4, "ny": 2, "alg": args.alg, "chunk": args.chunk, "prefetch": args.prefetch,
+         "T": 1 << args.log2t, "nx": 4, "ny": 2, "alg": args.alg, "chunk": args.chunk,
          "layout": "per-step (time-varying) model arrays" if not args.broadcast
                    else "time-invariant (broadcast) model, streamed y",
          "l2": "no flush needed: per-step inputs (7.0 GB f64) >> 126 MB L2",
@@ -190,7 +190,6 @@ def main() -> None:
     ap.add_argument("--log2t", type=int, default=24)
     ap.add_argument("--alg", default="DecoupledLookback")
     ap.add_argument("--chunk", type=int, default=64)
-    ap.add_argument("--prefetch", type=int, default=1)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--broadcast", action="store_true")
     ap.add_argument("--ref-log2t", type=int, default=18)
@@ -246,8 +245,7 @@ def run_psk(args) -> None:
     ys = torch.as_tensor(ys_np[lo:hi_in], dtype=tdt, device=dev)
     spec = psk.ScanSpec(psk.ScanAlg[args.alg], 16)
     stream = torch.cuda.Stream(device=dev)
-    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk, stream=stream,
-                         prefetch=args.prefetch)
+    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk, stream=stream)
 
     def step(profile: bool = False):
         be.set_profile(profile)
@@ -347,7 +345,7 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
                   h=pinned(H, T), d=pinned(np.zeros(2), T), r=pinned(R, T),
                   prior_mean=pinned(m0), prior_cov=pinned(P0), t=T)
     ys = pinned(ys_np)
-    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk, prefetch=args.prefetch)
+    be = psk.CudaBackend(local, mode="fast", chunk=args.chunk)
     h2d = sum(a.numel() * a.element_size() for a in (m.f, m.u, m.q, m.h, m.d, m.r, ys,
                                                      m.prior_mean, m.prior_cov))
     d2h = T * 20 * (8 if tdt == torch.float64 else 4)

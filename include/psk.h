@@ -98,8 +98,6 @@ int psk_set_mode(psk_ctx* ctx, int mode);
 int psk_set_chunk(psk_ctx* ctx, int chunk);
 /* Named tuning options of the fast path:
  *   "chunk"     steps folded per thread (same as psk_set_chunk)
- *   "prefetch"  per-step line prefetch of the next step's model blocks:
- *               0 off, 1 into L1, 2 into L2
  * Returns PSK_E_ARG for an unknown key or value. */
 int psk_set_option(psk_ctx* ctx, const char* key, int64_t value);
 /* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).

@@ -159,7 +159,7 @@ class CudaBackend:
     """
 
     def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 64,
-                 stream: Any = None, prefetch: int | None = None) -> None:
+                 stream: Any = None) -> None:
         L = _lib.lib()
         ctx = C.c_void_p()
         _check(L.psk_create(C.byref(ctx), int(device)))
@@ -167,8 +167,6 @@ class CudaBackend:
         self.device = int(device)
         self.set_mode(mode)
         self.set_chunk(chunk)
-        if prefetch is not None:
-            self.set_option("prefetch", prefetch)
         if stream is not None:
             self.set_stream(stream)
 

@@ -70,10 +70,12 @@ def build(verbose: bool = False) -> Path:
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}{p.stderr}")
+    # measurement tools (FMA peak, chunk-walk memory patterns): not the product
     tools = LIB / "libpsk_tools.so"
-    src = CSRC / "psk_peak.cu"
-    if not tools.exists() or src.stat().st_mtime > tools.stat().st_mtime:
-        cmd = [NVCC, *COMMON, "-shared", "-o", str(tools), str(src)]
+    srcs = [CSRC / "psk_peak.cu", CSRC / "psk_membench.cu"]
+    deps = srcs + [CSRC / "psk_stage.cuh", CSRC / "psk_mat.cuh"]
+    if not tools.exists() or any(d.stat().st_mtime > tools.stat().st_mtime for d in deps):
+        cmd = [NVCC, *COMMON, "-shared", "-o", str(tools), *map(str, srcs)]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"tools build failed:\n{p.stdout}{p.stderr}")

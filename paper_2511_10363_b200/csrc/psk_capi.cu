@@ -37,7 +37,6 @@ struct psk_ctx {
   cudaStream_t stream = nullptr;
   int mode = PSK_MODE_FAST;
   long long chunk = 64;
-  int prefetch = 1;
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
@@ -123,34 +122,35 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     if (!f[i].src) return fail(PSK_E_ARG, std::string("null model field ") + f[i].name);
     long long st = f[i].stride < 0 ? f[i].block : f[i].stride;
     const size_t bb = sizeof(S) * (size_t)f[i].block;
-    // vector width used by the device loads for this block (psk_mat.cuh load)
-    const size_t al = bb % 16 == 0 ? 16 : (bb % 8 == 0 ? 8 : sizeof(S));
-    const bool dense_ok = !host &&
-                          (reinterpret_cast<uintptr_t>(f[i].src) % al) == 0 &&
-                          ((size_t)st * sizeof(S)) % al == 0;
+    // Device arrays are used in place when the TMA stage (psk_stage.cuh) can
+    // read them: 16-byte aligned base, per-step pitch a multiple of 16 bytes,
+    // and blocks that are whole 16-byte rows (the stage reads rounded rows).
+    const bool dense_ok = !host && bb % 16 == 0 &&
+                          (reinterpret_cast<uintptr_t>(f[i].src) % 16) == 0 &&
+                          ((size_t)st * sizeof(S)) % 16 == 0;
     if (dense_ok) {
       outp[i] = static_cast<const S*>(f[i].src);
       outs[i] = st;
       continue;
     }
-    // pack: one block if broadcast, else T blocks at the given stride (plus the
-    // boundary transition of a sharded run for f/u/q)
+    // pack: one block if broadcast, else T blocks (plus the boundary
+    // transition of a sharded run for f/u/q) at a 16-byte-rounded pitch
     const long long nblk =
         st == 0 ? 1 : (T > 0 ? T : 1) + ((i == 0 || i == 1 || i == 2) ? extra_fuq : 0);
-    S* dst = static_cast<S*>(ctx_alloc(sizeof(S) * (size_t)(nblk * f[i].block), ctx));
+    const size_t pb = (bb + 15) / 16 * 16;
+    S* dst = static_cast<S*>(ctx_alloc(pb * (size_t)nblk, ctx));
     if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
     const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     cudaError_t e;
-    if (st == 0 || st == f[i].block) {
-      e = cudaMemcpyAsync(dst, f[i].src, sizeof(S) * (size_t)(nblk * f[i].block), kind,
-                          ctx->stream);
+    if (st != 0 && pb == bb && st == f[i].block) {
+      e = cudaMemcpyAsync(dst, f[i].src, bb * (size_t)nblk, kind, ctx->stream);
     } else {
-      e = cudaMemcpy2DAsync(dst, bb, f[i].src, sizeof(S) * (size_t)st, bb, (size_t)nblk,
-                            kind, ctx->stream);
+      e = cudaMemcpy2DAsync(dst, pb, f[i].src, st == 0 ? bb : sizeof(S) * (size_t)st, bb,
+                            (size_t)nblk, kind, ctx->stream);
     }
     if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("model copy: ") + cuda_msg(e));
     outp[i] = dst;
-    outs[i] = st == 0 ? 0 : f[i].block;
+    outs[i] = st == 0 ? 0 : (long long)(pb / sizeof(S));
   }
   // prior
   const void* pm = m->prior_mean;
@@ -221,7 +221,6 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     a.alg = alg;
     a.sengupta_n = sengupta_n;
     a.chunk = ctx->chunk;
-    a.prefetch = ctx->prefetch;
     st = fast_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
     if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
     if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
@@ -307,7 +306,6 @@ int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   a.alg = alg;
   a.sengupta_n = sn;
   a.chunk = ctx->chunk;
-  a.prefetch = ctx->prefetch;
   if (phase != 0 && phase != 2) {  // finishes reuse the scan spec of the reduce
     a.alg = ctx->shard_alg;
     a.sengupta_n = ctx->shard_sn;
@@ -482,9 +480,6 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   if (k == "chunk") {
     if (value < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
     c->chunk = value;
-  } else if (k == "prefetch") {
-    if (value < 0 || value > 2) return fail(PSK_E_ARG, "prefetch must be 0, 1 or 2");
-    c->prefetch = (int)value;
   } else {
     return fail(PSK_E_ARG, "unknown option " + k);
   }

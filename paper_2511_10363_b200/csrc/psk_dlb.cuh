@@ -1,18 +1,30 @@
 // psk_dlb.cuh -- single-pass decoupled look-back scan (NEW: not in the
 // reference; appended as ScanAlg value 6 after SenguptaB, scan.hpp:32-39).
 //
-// Each CTA takes the next tile of TILE elements from a global ticket counter
-// (forward progress: every predecessor tile is running or done), scans it in
-// shared memory with a work-efficient up-sweep / Ladner-Fischer down-sweep
-// (the pattern of scan.hpp:261-279 and 343-367 applied to the tile),
-// publishes its aggregate (flag A) immediately, looks back over the
-// predecessors' published aggregates / inclusive prefixes (non-commutative:
-// predecessors are folded on the LEFT), publishes its inclusive prefix (flag
-// P) and applies the exclusive prefix to its elements.  The element payload
-// (56 scalars at nx=4) is far wider than an atomic, so it is published as
-// payload + release flag and read back with L1-bypassing loads after an
-// acquire load of the flag.  Reverse scans use the Reversed<E> index map with
-// flipped operands (scan.hpp:149-177).
+// One CTA of kDlbThreads threads scans a tile of kDlbThreads * K consecutive
+// elements (K per thread, chosen on the host so that all tiles of a typical
+// chunk scan are resident in one wave):
+//   1. tile ticket from a global counter (forward progress: every tile with a
+//      smaller ticket is running or done);
+//   2. each thread folds its K consecutive elements serially (work-efficient);
+//   3. the 128 thread aggregates are scanned in shared memory (up-sweep +
+//      Ladner-Fischer down-sweep, the index maps of scan.hpp:261-279 and
+//      343-367 applied to the tile); the thread-inclusive prefixes are parked
+//      in global scratch;
+//   4. the tile aggregate is published (flag A; tile 0 publishes its inclusive
+//      prefix, flag P, directly);
+//   5. look-back, CTA-parallel: thread i inspects predecessor tile base-i of a
+//      128-wide window, the nearest P in the window bounds it, the window's
+//      aggregates (+ that P) are reduced in time order by a 7-level tree in
+//      shared memory and folded onto the LEFT of the running exclusive prefix
+//      (non-commutative).  Without a P the window slides back by 128 tiles;
+//   6. the inclusive prefix of the tile is published (flag P) and every thread
+//      re-folds its K elements from (exclusive tile prefix (x) thread
+//      exclusive prefix), writing the inclusive prefixes in place.
+// The element payload (56 scalars at nx=4) is far wider than an atomic, so it
+// is published as payload + release flag and read with L1-bypassing loads
+// after an acquire load of the flag.  Reverse scans use the Reversed<E> index
+// map with flipped operands (scan.hpp:149-177).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -21,7 +33,10 @@
 
 namespace psk {
 
-constexpr int kDlbTile = 128;
+constexpr int kDlbThreads = 128;
+constexpr int kDlbLevels = 7;  // log2(kDlbThreads)
+static_assert((1 << kDlbLevels) == kDlbThreads, "CTA must be 2^kDlbLevels threads");
+constexpr int kDlbSlots = kDlbThreads + 2;  // + exclusive tile prefix + scratch
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -32,112 +47,197 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// state layout: [ticket u32 | pad][flags u32 x ntiles][agg S x size x ntiles]
-//               [incl S x size x ntiles]
+// elements per thread: the smallest K >= 1 that keeps the tile count within
+// about one resident wave (148 SMs x 3 CTAs), capped at 16
+inline int dlb_per_thread(long long n) {
+  const long long target = 148LL * 3 * kDlbThreads;
+  long long k = (n + target - 1) / target;
+  if (k < 1) k = 1;
+  if (k > 16) k = 16;
+  return (int)k;
+}
+inline long long dlb_tiles(long long n) {
+  const long long per = (long long)kDlbThreads * dlb_per_thread(n);
+  return (n + per - 1) / per;
+}
+__host__ __device__ inline size_t dlb_head_bytes(long long ntiles) {
+  return 256 + ((size_t)ntiles * 4 + 255) / 256 * 256;
+}
+// state layout: [ticket u32 | pad][flags u32 x ntiles][agg FS x ntiles]
+//               [incl FS x ntiles][thread prefixes FS x ntiles*kDlbThreads]
 template <typename S, int NX>
 inline size_t dlb_state_bytes(long long n) {
-  const long long nt = (n + kDlbTile - 1) / kDlbTile;
-  const size_t head = 256 + ((size_t)nt * 4 + 255) / 256 * 256;
-  return head + 2 * sizeof(S) * (size_t)(3 * NX * NX + 2 * NX) * (size_t)nt;
+  const long long nt = dlb_tiles(n);
+  const size_t fs = (size_t)(3 * NX * NX + 2 * NX);
+  return dlb_head_bytes(nt) + sizeof(S) * fs * (size_t)nt * (2 + kDlbThreads);
 }
 
 template <class Ops>
-__global__ void __launch_bounds__(kDlbTile)
+__global__ void __launch_bounds__(kDlbThreads)
     k_dlb(Ops ops, typename Ops::S* buf, long long n, int rev, char* state,
-          long long ntiles) {
+          long long ntiles, int per) {
   using S = typename Ops::S;
-  constexpr int FS = Ops::kSize;
   extern __shared__ __align__(16) unsigned char dlb_smem[];
   S* sm = reinterpret_cast<S*>(dlb_smem);
-  const int cap = kDlbTile + 2;  // slot kDlbTile = exclusive prefix, +1 scratch
-  const ElemBuf<S> sb{sm, cap, cap, 0};
+  const ElemBuf<S> sb{sm, kDlbSlots, kDlbSlots, 0};
   const ElemBuf<S> gb{buf, n, n, 0};
   unsigned* ticket = reinterpret_cast<unsigned*>(state);
   unsigned* flags = reinterpret_cast<unsigned*>(state + 256);
-  const size_t head = 256 + ((size_t)ntiles * 4 + 255) / 256 * 256;
-  S* pagg = reinterpret_cast<S*>(state + head);
-  S* pincl = pagg + (size_t)FS * ntiles;
+  S* pagg = reinterpret_cast<S*>(state + dlb_head_bytes(ntiles));
+  S* pincl = pagg + (size_t)Ops::kSize * ntiles;
+  S* pthr = pincl + (size_t)Ops::kSize * ntiles;
+  const long long thr_cap = ntiles * kDlbThreads;
+  const ElemBuf<S> ab{pagg, ntiles, ntiles, 0};
+  const ElemBuf<S> ib{pincl, ntiles, ntiles, 0};
+  const ElemBuf<S> tb{pthr, thr_cap, thr_cap, 0};
+  constexpr int kExcl = kDlbThreads, kTmp = kDlbThreads + 1;
   __shared__ unsigned s_tile;
+  __shared__ int s_stop;
   const int t = threadIdx.x;
   if (t == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const long long tile = s_tile;
-  const long long g = tile * kDlbTile + t;  // logical index
-  // logical (x) on the shared tile: reversed scans flip the operands
-  auto lcomb = [&](int dst, int l, int r) {
+  // logical (x) on (buffer, index) pairs: reversed scans flip the operands
+  auto lcomb = [&](const ElemBuf<S>& d, long long di, const ElemBuf<S>& l, long long li,
+                   const ElemBuf<S>& r, long long ri) {
     if (!rev)
-      ops.combine(sb, dst, sb, l, sb, r);
+      ops.combine(d, di, l, li, r, ri);
     else
-      ops.combine(sb, dst, sb, r, sb, l);
+      ops.combine(d, di, r, ri, l, li);
   };
-  if (g < n) {
-    const long long p = rev ? n - 1 - g : g;
-    ops.assign(sb, t, gb, p);
+  auto phys = [&](long long g) { return rev ? n - 1 - g : g; };
+
+  // 2. serial fold of this thread's K consecutive elements into slot t
+  const long long g0 = (tile * kDlbThreads + t) * per;
+  const long long g1 = g0 + per < n ? g0 + per : n;
+  if (g0 < n) {
+    ops.assign(sb, t, gb, phys(g0));
+    for (long long g = g0 + 1; g < g1; ++g) lcomb(sb, t, sb, t, gb, phys(g));
   } else {
     ops.identity(sb, t);
   }
   __syncthreads();
-  // tile scan: up-sweep then Ladner-Fischer down-sweep
-  constexpr int kLevels = 7;  // log2(kDlbTile)
-  static_assert((1 << kLevels) == kDlbTile, "tile must be 2^kLevels");
+  // 3. tile scan of the thread aggregates: up-sweep, then Ladner-Fischer down
 #pragma unroll 1
-  for (int d = 0; d < kLevels; ++d) {
+  for (int d = 0; d < kDlbLevels; ++d) {
     const int d1 = 1 << d, d2 = d1 << 1;
-    if (t < kDlbTile / d2) {
+    if (t < kDlbThreads / d2) {
       const int j = t * d2 + d1 - 1, k = t * d2 + d2 - 1;
-      lcomb(k, j, k);
+      lcomb(sb, k, sb, j, sb, k);
     }
     __syncthreads();
   }
 #pragma unroll 1
-  for (int d = kLevels - 1; d >= 0; --d) {
-    const int d1 = 1 << d, d2 = d1 << 1, blocks = kDlbTile / d2;
+  for (int d = kDlbLevels - 1; d >= 0; --d) {
+    const int d1 = 1 << d, d2 = d1 << 1, blocks = kDlbThreads / d2;
     if (blocks > 1 && t < blocks - 1) {
       const int i = (t + 1) * d2 - 1, j = i + d1;
-      lcomb(j, i, j);
+      lcomb(sb, j, sb, i, sb, j);
     }
     __syncthreads();
   }
-  // publish + look-back (one thread; the payload is FS scalars)
-  const ElemBuf<S> ab{pagg, ntiles, ntiles, 0};
-  const ElemBuf<S> ib{pincl, ntiles, ntiles, 0};
+  // 4. publish the tile aggregate (tile 0: its inclusive prefix); park the
+  // thread-inclusive prefixes in global scratch (the slots become the window)
+  constexpr int last = kDlbThreads - 1;
+  if (tile > 0) ops.assign(tb, tile * kDlbThreads + t, sb, t);
   if (t == 0) {
-    const int last = kDlbTile - 1;
-    if (tile == 0) {
-      ops.assign(ib, tile, sb, last);
-      __threadfence();
-      st_release(flags + tile, 2u);
-    } else {
-      ops.assign(ab, tile, sb, last);
-      __threadfence();
-      st_release(flags + tile, 1u);
-      bool have = false;
-      for (long long pt = tile - 1; pt >= 0; --pt) {
-        unsigned f;
+    ops.assign(tile == 0 ? ib : ab, tile, sb, last);
+    __threadfence();
+    st_release(flags + tile, tile == 0 ? 2u : 1u);
+    if (tile > 0) ops.assign(sb, kTmp, sb, last);  // keep the tile aggregate
+  }
+  // tile 0: the tile prefix is the identity; slot t already holds the
+  // thread-inclusive prefix (shifted to thread-exclusive below)
+  if (tile > 0) {
+    // 5. look-back over windows of kDlbThreads predecessors
+    bool have = false;
+    long long base = tile - 1;
+#pragma unroll 1
+    while (true) {
+      if (t == 0) s_stop = kDlbThreads;
+      __syncthreads();
+      const long long pt = base - t;
+      unsigned f = 0;
+      if (pt >= 0) {
         while ((f = ld_acquire(flags + pt)) == 0u) {
         }
-        const S* src = f == 2u ? pincl : pagg;
-        for (int c = 0; c < FS; ++c)
-          sm[c * cap + kDlbTile + 1] = __ldcg(src + (size_t)c * ntiles + pt);
-        if (!have) {
-          ops.assign(sb, kDlbTile, sb, kDlbTile + 1);
-          have = true;
-        } else {
-          lcomb(kDlbTile, kDlbTile + 1, kDlbTile);  // X_pt (x) excl
-        }
-        if (f == 2u) break;
+        if (f == 2u) atomicMin(&s_stop, t);
       }
-      lcomb(kDlbTile + 1, kDlbTile, last);  // inclusive = excl (x) aggregate
-      ops.assign(ib, tile, sb, kDlbTile + 1);
+      __syncthreads();
+      const int stop = s_stop;  // nearest P (kDlbThreads: none in the window)
+      // slot (last - t) holds predecessor base - t: time order ascending
+      const int slot = last - t;
+      if (t <= stop && pt >= 0) {
+        const S* src = f == 2u ? pincl : pagg;
+        for (int c = 0; c < Ops::kSize; ++c)
+          sm[c * kDlbSlots + slot] = __ldcg(src + (size_t)c * ntiles + pt);
+      } else {
+        ops.identity(sb, slot);
+      }
+      __syncthreads();
+      // ordered tree reduction of the window into slot 0
+#pragma unroll 1
+      for (int d = 0; d < kDlbLevels; ++d) {
+        const int s = 1 << d;
+        if ((t & (2 * s - 1)) == 0) lcomb(sb, t, sb, t, sb, t + s);
+        __syncthreads();
+      }
+      if (t == 0) {
+        if (!have)
+          ops.assign(sb, kExcl, sb, 0);
+        else
+          lcomb(sb, kExcl, sb, 0, sb, kExcl);  // window is earlier: on the left
+      }
+      have = true;
+      __syncthreads();
+      if (stop < kDlbThreads || base - kDlbThreads < 0) break;
+      base -= kDlbThreads;
+    }
+    // 6. publish the inclusive prefix of the tile
+    if (t == 0) {
+      lcomb(sb, kTmp, sb, kExcl, sb, kTmp);
+      ops.assign(ib, tile, sb, kTmp);
       __threadfence();
       st_release(flags + tile, 2u);
     }
+    __syncthreads();
   }
-  __syncthreads();
-  if (tile > 0) lcomb(t, kDlbTile, t);
-  if (g < n) {
-    const long long p = rev ? n - 1 - g : g;
-    ops.assign(gb, p, sb, t);
+  // thread-exclusive prefix: (tile exclusive) (x) (thread-inclusive of t-1)
+  if (tile == 0) {
+    // shift slot t-1 -> t through registers (all reads before all writes)
+    S v[Ops::kSize];
+    if (t > 0) {
+#pragma unroll
+      for (int c = 0; c < Ops::kSize; ++c) v[c] = sm[c * kDlbSlots + t - 1];
+    }
+    __syncthreads();
+    if (t > 0) {
+#pragma unroll
+      for (int c = 0; c < Ops::kSize; ++c) sm[c * kDlbSlots + t] = v[c];
+    }
+    __syncthreads();
+    if (g0 < n) {
+      long long g = g0;
+      if (t == 0) {  // no prefix: the first element is its own prefix
+        ++g;
+        ops.assign(sb, t, gb, phys(g0));
+      }
+      for (; g < g1; ++g) {
+        lcomb(sb, t, sb, t, gb, phys(g));
+        ops.assign(gb, phys(g), sb, t);
+      }
+    }
+  } else {
+    if (g0 < n) {
+      if (t == 0)
+        ops.assign(sb, t, sb, kExcl);
+      else
+        lcomb(sb, t, sb, kExcl, tb, tile * kDlbThreads + t - 1);
+      for (long long g = g0; g < g1; ++g) {
+        lcomb(sb, t, sb, t, gb, phys(g));
+        ops.assign(gb, phys(g), sb, t);
+      }
+    }
   }
 }
 
@@ -146,18 +246,14 @@ void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf,
               long long n, int rev, typename Ops::S* /*unused*/, void* state) {
   using S = typename Ops::S;
   if (n <= 0) return;
-  const long long ntiles = (n + kDlbTile - 1) / kDlbTile;
-  const size_t head = 256 + ((size_t)ntiles * 4 + 255) / 256 * 256;
-  cudaMemsetAsync(state, 0, head, L.stream);
-  const size_t smem = sizeof(S) * (size_t)Ops::kSize * (kDlbTile + 2);
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_dlb<Ops>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr_set = true;
-  }
-  k_dlb<Ops><<<(unsigned)ntiles, kDlbTile, smem, L.stream>>>(
-      ops, buf, n, rev, reinterpret_cast<char*>(state), ntiles);
+  const int per = dlb_per_thread(n);
+  const long long ntiles = dlb_tiles(n);
+  cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
+  const size_t smem = sizeof(S) * (size_t)Ops::kSize * kDlbSlots;
+  // the attribute is per device: set it on every call (cheap)
+  cudaFuncSetAttribute(k_dlb<Ops>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_dlb<Ops><<<(unsigned)ntiles, kDlbThreads, smem, L.stream>>>(
+      ops, buf, n, rev, reinterpret_cast<char*>(state), ntiles, per);
   L.count("chunk_scan_dlb");
 }
 

@@ -54,7 +54,6 @@ struct FastArgs {
   int alg = 3;          // psk_alg
   unsigned long long sengupta_n = 1;
   long long chunk = 32;
-  int prefetch = 0;     // per-step line prefetch: 0 off, 1 L1, 2 L2
 };
 template <typename S>
 bool fast_supported(int nx, int ny);

@@ -50,6 +50,54 @@ struct SLayout {
                        size = 2 * NX * NX + NX;
 };
 
+// Per-step smoothing elements (E, g, L) written by the PRTS filter finish and
+// consumed by the smoother finish (an internal buffer, so its layout is free):
+// L is symmetric and only its upper triangle is kept (NX(NX+1)/2 scalars).
+// Step j of chunk c lives at comp * cap ... with index (j * kSize + comp) *
+// cap + c: consecutive chunks (= consecutive threads) are adjacent, so every
+// access is a coalesced 32-lane transaction.
+template <int NX>
+struct EglLayout {
+  static constexpr int E = 0, g = NX * NX, L = NX * NX + NX,
+                       size = NX * NX + NX + NX * (NX + 1) / 2;
+};
+template <typename S, int NX>
+__device__ __forceinline__ void egl_store(S* p, long long cap, const SElem<S, NX>& e) {
+  using Lo = EglLayout<NX>;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) __stcs(p + (Lo::E + i * NX + j) * cap, e.E.a[i][j]);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) __stcs(p + (Lo::g + i) * cap, e.g.a[i][0]);
+  int q = Lo::L;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) __stcs(p + (q++) * cap, e.L.a[i][j]);
+}
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> egl_load(const S* p, long long cap) {
+  using Lo = EglLayout<NX>;
+  SElem<S, NX> e;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = 0; j < NX; ++j) e.E.a[i][j] = __ldcs(p + (Lo::E + i * NX + j) * cap);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e.g.a[i][0] = __ldcs(p + (Lo::g + i) * cap);
+  int q = Lo::L;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) {
+      const S v = __ldcs(p + (q++) * cap);
+      e.L.a[i][j] = v;
+      e.L.a[j][i] = v;
+    }
+  return e;
+}
+
 template <typename S, int NX>
 __device__ __forceinline__ FElem<S, NX> fe_load(const S* p, long long cap,
                                                 long long i) {
@@ -393,46 +441,107 @@ __device__ __forceinline__ void filter_apply(Vec<S, NX>& x, Mat<S, NX, NX>& P,
 
 // ============================================================================
 // Staged per-step kernels.  Each thread owns one chunk of consecutive steps;
-// the per-step model blocks of step k+1 (k-1 when walking backwards) are
-// fetched into shared memory with cp.async while step k is computed.
-// Blocks are one warp (NT = 32) so that ~8 CTAs of 226-register threads fit
-// per SM together with their 2 x 13 KB stages.
+// the CTA's step j+1 is fetched into shared memory by TMA (psk_stage.cuh)
+// while step j is computed, double-buffered.  At 255 registers per FP64
+// thread only 8 warps fit per SM -- far too few to hide HBM latency with
+// plain loads (profiles/r01_v0: long-scoreboard stalls dominated); the stage
+// keeps a whole step of the CTA in flight instead.
 // ============================================================================
-constexpr int kStageNT = 128;
 
-__device__ __forceinline__ void prefetch_line(const void* p, int pf) {
-  if (pf == 1)
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-  else if (pf == 2)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// Step view: per-step model blocks read straight from global memory (each
-// block is one thread's contiguous 16..128 B; L1 serves the rest of a line).
-template <typename S>
-struct FStep {
+// This thread's view of one step: the TMA stage, or global memory for a
+// broadcast field and for the ragged tail chunk (which the tensor maps --
+// full chunks only -- do not cover).
+template <typename S, int NX, int NY>
+struct FilterStage {
+  using In = FilterTma<S, NX, NY>;
+  const unsigned char* st;
+  int t;
+  bool direct;
   const ModelView<S>* m;
   long long k;
+  __device__ __forceinline__ Mat<S, NX, NX> F() const {
+    return direct || m->sf == 0 ? load<S, NX, NX>(m->F(k))
+                                : tma_get<typename In::F, S, NX, NX>(st, t);
+  }
+  __device__ __forceinline__ Vec<S, NX> u() const {
+    return direct || m->su == 0 ? load<S, NX, 1>(m->U(k))
+                                : tma_get<typename In::u, S, NX, 1>(st, t);
+  }
+  __device__ __forceinline__ Mat<S, NX, NX> Q() const {
+    return direct || m->sq == 0 ? load<S, NX, NX>(m->Q(k))
+                                : tma_get<typename In::Q, S, NX, NX>(st, t);
+  }
+  __device__ __forceinline__ Meas<S, NX, NY> meas() const {
+    Meas<S, NX, NY> z;
+    z.H = direct || m->sh == 0 ? load<S, NY, NX>(m->H(k))
+                               : tma_get<typename In::H, S, NY, NX>(st, t);
+    z.d = direct || m->sd == 0 ? load<S, NY, 1>(m->D(k))
+                               : tma_get<typename In::d, S, NY, 1>(st, t);
+    z.R = direct || m->sr == 0 ? load<S, NY, NY>(m->R(k))
+                               : tma_get<typename In::R, S, NY, NY>(st, t);
+    z.y = direct || m->sy == 0 ? load<S, NY, 1>(m->Y(k))
+                               : tma_get<typename In::y, S, NY, 1>(st, t);
+    return z;
+  }
 };
 
-// prefetch the lines of step k's model blocks (pf: 0 off, 1 L1, 2 L2)
-template <typename S, int NX, int NY>
-__device__ __forceinline__ void prefetch_filter_in(const ModelView<S>& m, long long k, int pf) {
-  if (pf == 0) return;
-  prefetch_line(m.F(k), pf);
-  prefetch_line(m.Q(k), pf);
-  prefetch_line(m.U(k), pf);
-  prefetch_line(m.H(k), pf);
-  prefetch_line(m.D(k), pf);
-  prefetch_line(m.R(k), pf);
-  prefetch_line(m.Y(k), pf);
+// Double-buffered TMA walk over this thread's chunk c = steps [k0, k1).
+// body(k, stage) sees step k's inputs; step k+1's are in flight.  The walk
+// is CTA-uniform (every thread of the CTA must call it: block barriers), of
+// length min(L, T - first step of the CTA).  `nfull` = number of complete
+// chunks (the extent of the tensor maps).
+template <typename S, int NX, int NY, class Body>
+__device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const StageMaps& maps,
+                                            const ModelView<S>& m, long long L, long long nfull,
+                                            long long k0, long long k1, Body&& body) {
+  using In = FilterTma<S, NX, NY>;
+  using St = FilterStage<S, NX, NY>;
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * In::stage);
+  const int t = threadIdx.x;
+  const long long cta0 = (long long)blockIdx.x * kStageNT;  // first chunk of the CTA
+  const bool tma = cta0 < nfull;                            // CTA-uniform
+  const long long jn = min(L, m.t - cta0 * L);
+  const bool direct = !tma || cta0 + t >= nfull;
+  auto issue = [&](int s, long long j) {
+    fence_proxy_async();  // generic reads of this stage (last use) before the refill
+    mbar_expect_tx(&bars[s], maps.tx);
+#pragma unroll
+    for (int f = 0; f < 7; ++f)
+      if (maps.use[f])
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j, (int)cta0,
+                    &bars[s]);
+  };
+  if (tma && t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+    issue(0, 0);
+  }
+  __syncthreads();
+  for (long long j = 0; j < jn; ++j) {
+    const int s = (int)(j & 1);
+    if (tma && t == 0 && j + 1 < jn) issue(s ^ 1, j + 1);
+    if (tma) mbar_wait(&bars[s], (unsigned)((j >> 1) & 1));
+    if (k0 + j < k1) body(k0 + j, St{sm + s * In::stage, t, direct, &m, k0 + j});
+    __syncthreads();  // stage s is refilled by the next iteration's issue
+  }
 }
-// predict with (F, u, Q)_k + update with y_k
+
+// Filtering element of step k from its staged inputs (make_filter_element,
+// kalman_elems.hpp:97-147, k > 1)
 template <typename S, int NX, int NY>
-__device__ __forceinline__ void kf_step(Vec<S, NX>& x, Mat<S, NX, NX>& P,
-                                        const ModelView<S>& m, long long k, unsigned& err) {
-  kf_predict(x, P, m, k);
-  kf_update(x, P, load_meas<S, NX, NY>(m, k), err);
+__device__ __forceinline__ FElem<S, NX> make_filter_elem(const FilterStage<S, NX, NY>& in,
+                                                         unsigned& err) {
+  FElem<S, NX> e;
+  e.A = in.F();
+  e.b = in.u();
+  e.C = in.Q();
+  e.eta = zeros<S, NX, 1>();
+  e.J = zeros<S, NX, NX>();
+  cond_update(e, in.meas(), err);
+  return e;
 }
 
 // Smoothing element of step i from the filtered (x, P)_i and the transition
@@ -477,43 +586,38 @@ __device__ __forceinline__ SElem<S, NX> terminal_elem(const Vec<S, NX>& x,
 
 // reduce: chunk c = steps [c L, min(c L + L, T)) -> one filtering element
 template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(kStageNT)
-    k_filter_reduce(ModelView<S> m, long long L, long long nchunks, S* agg,
-                    long long cap, int pf, unsigned* err) {
+__global__ void __launch_bounds__(kStageNT, 2)
+    k_filter_reduce(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
+                    long long nchunks, long long nfull, S* agg, long long cap, unsigned* err) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
+  const bool live = c < nchunks;  // idle threads stay for the block barriers
   unsigned e = 0;
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, m.t);
-  FElem<S, NX> a;
-  if (k0 == 0 && m.prior_first) {
-    // a_1 absorbs the prior (kalman_elems.hpp:68-96): A = 0 and the prefix
-    // is the filtered state itself, so run the chunk in state form.
-    Vec<S, NX> x = load<S, NX, 1>(m.m0);
-    Mat<S, NX, NX> P = load<S, NX, NX>(m.p0);
-    for (long long k = k0; k < k1; ++k) {
-      if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
-      kf_step<S, NX, NY>(x, P, m, k, e);
-    }
+  using St = FilterStage<S, NX, NY>;
+  // Every step is composed onto the running element by the conditional
+  // Kalman recursion.  From the identity (I, 0, 0, 0, 0) the first step gives
+  // exactly make_filter_element (kalman_elems.hpp:97-147); the chunk holding
+  // step 1 starts from the prior in state form (A = 0, b = m0, C = P0), which
+  // absorbs it as a_1 does (kalman_elems.hpp:68-96) -- A, eta and J then stay
+  // 0 and the element is the filtered state itself.
+  FElem<S, NX> a = fe_identity<S, NX>();
+  if (live && k0 == 0 && m.prior_first) {
     a.A = zeros<S, NX, NX>();
-    a.b = x;
-    a.C = P;
-    a.eta = zeros<S, NX, 1>();
-    a.J = zeros<S, NX, NX>();
-  } else {
-    a = make_filter_elem<S, NX, NY>(m, k0, e);
-    for (long long k = k0 + 1; k < k1; ++k) {
-      if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
-      // predict the conditional: (F A, F b + u, F C F^T + Q), then update
-      const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
-      a.A = mul(F, a.A);
-      a.b = mul_add(F, a.b, load<S, NX, 1>(m.U(k)));
-      const Mat<S, NX, NX> fc = mul(F, a.C);
-      a.C = mul_nt_sym_add(fc, F, load<S, NX, NX>(m.Q(k)));
-      cond_update(a, load_meas<S, NX, NY>(m, k), e);
-    }
+    a.b = load<S, NX, 1>(m.m0);
+    a.C = load<S, NX, NX>(m.p0);
   }
-  fe_store(agg, cap, c, a);
+  staged_walk<S, NX, NY>(fsm, maps, m, L, nfull, k0, k1, [&](long long, const St& in) {
+    // predict the conditional: (F A, F b + u, F C F^T + Q), then update
+    const Mat<S, NX, NX> F = in.F();
+    a.A = mul(F, a.A);
+    a.b = mul_add(F, a.b, in.u());
+    const Mat<S, NX, NX> fc = mul(F, a.C);
+    a.C = mul_nt_sym_add(fc, F, in.Q());
+    cond_update(a, in.meas(), e);
+  });
+  if (live) fe_store(agg, cap, c, a);
   if (e) atomicOr(err, e);
 }
 
@@ -545,46 +649,54 @@ __device__ __forceinline__ void filter_incoming(const ModelView<S>& m, long long
 }
 
 // finish: sequential Kalman filter over the chunk from the carried prefix.
-// With `sagg` non-null (PRTS) the same pass also folds the chunk's smoothing
-// element e_{k0} (x) ... (x) e_{k1-1} (Lemma 2 is associative, so the chunk
-// element is built forwards): e_{k-1} needs the filtered state of step k-1
-// and the transition (F, Q, u)_k that the filter loads for step k anyway.
+// PKF/PTFS (egl == nullptr): writes the filtered stats.  PRTS (egl non-null):
+// the filtered stats are not needed by the caller, only the smoother is --
+// the pass writes the per-step smoothing elements e_k (kalman_elems.hpp:
+// 151-193) instead, and folds the chunk's smoothing element e_{k0} (x) ... (x)
+// e_{k1-1} into `sagg` (Lemma 2 is associative, so the chunk element is built
+// forwards).  e_{k-1} needs the filtered state of step k-1 and the
+// transition (F, Q, u)_k that the filter loads for step k anyway.
 template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(kStageNT)
-    k_filter_finish(ModelView<S> m, long long L, long long nchunks, const S* pre,
-                    long long pre_cap, const S* carry, S* mean, S* cov, S* sagg,
-                    long long scap, int pf, unsigned* err) {
+__global__ void __launch_bounds__(kStageNT, 2)
+    k_filter_finish(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
+                    long long nchunks, long long nfull, const S* pre, long long pre_cap,
+                    const S* carry, S* mean, S* cov, S* sagg, long long scap, S* egl,
+                    unsigned* err) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
+  const bool live = c < nchunks;  // idle threads stay for the block barriers
   unsigned e = 0;
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, m.t);
-  Vec<S, NX> x;
-  Mat<S, NX, NX> P;
-  filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
+  constexpr int ES = EglLayout<NX>::size;
+  using St = FilterStage<S, NX, NY>;
+  Vec<S, NX> x = zeros<S, NX, 1>();
+  Mat<S, NX, NX> P = zeros<S, NX, NX>();
+  if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
   SElem<S, NX> sa;
-  for (long long k = k0; k < k1; ++k) {
-    if (k + 1 < k1) prefetch_filter_in<S, NX, NY>(m, k + 1, pf);
-    const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
-    const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
-    const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
-    if (sagg != nullptr && k > k0) {  // (x, P) still hold the filtered step k-1
+  staged_walk<S, NX, NY>(fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
+    const Mat<S, NX, NX> F = in.F();
+    const Mat<S, NX, NX> Q = in.Q();
+    const Vec<S, NX> u = in.u();
+    if (egl != nullptr && k > k0) {  // (x, P) still hold the filtered step k-1
       const SElem<S, NX> ek = smoother_elem(x, P, F, Q, u, e);
+      egl_store(egl + (k - 1 - k0) * ES * scap + c, scap, ek);
       sa = k - 1 == k0 ? ek : smoother_combine(sa, ek);
     }
     x = mul_add(F, x, u);
     const Mat<S, NX, NX> fp = mul(F, P);
     P = mul_nt_sym_add(fp, F, Q);
-    kf_update(x, P, load_meas<S, NX, NY>(m, k), e);
-    store_state(mean, cov, k, x, P);
-  }
-  if (sagg != nullptr) {  // element of the chunk's last step
+    kf_update(x, P, in.meas(), e);
+    if (egl == nullptr) store_state(mean, cov, k, x, P);
+  });
+  if (live && egl != nullptr) {  // element of the chunk's last step
     SElem<S, NX> ek;
     if (k1 - 1 == m.last_step)
       ek = terminal_elem(x, P);
     else
       ek = smoother_elem(x, P, load<S, NX, NX>(m.F(k1)), load<S, NX, NX>(m.Q(k1)),
                          load<S, NX, 1>(m.U(k1)), e);
+    egl_store(egl + (k1 - 1 - k0) * ES * scap + c, scap, ek);
     sa = k1 - 1 == k0 ? ek : smoother_combine(sa, ek);
     se_store(sagg, scap, c, sa);
   }
@@ -595,70 +707,25 @@ __global__ void __launch_bounds__(kStageNT)
 // RTS smoother kernels (reverse direction)
 // ============================================================================
 
-template <typename S, int NX>
-__device__ __forceinline__ void prefetch_smoother_in(const ModelView<S>& m, const S* mean,
-                                                     const S* cov, long long i, int pf) {
-  if (pf == 0) return;
-  prefetch_line(mean + i * NX, pf);
-  prefetch_line(cov + i * NX * NX, pf);
-  if (i != m.last_step) {
-    prefetch_line(m.F(i + 1), pf);
-    prefetch_line(m.Q(i + 1), pf);
-    prefetch_line(m.U(i + 1), pf);
-  }
-}
-template <typename S, int NX>
-__device__ __forceinline__ SElem<S, NX> smoother_elem_at(const ModelView<S>& m, long long i,
-                                                         const Vec<S, NX>& x,
-                                                         const Mat<S, NX, NX>& P,
-                                                         unsigned& e) {
-  if (i == m.last_step) return terminal_elem(x, P);
-  return smoother_elem(x, P, load<S, NX, NX>(m.F(i + 1)), load<S, NX, NX>(m.Q(i + 1)),
-                       load<S, NX, 1>(m.U(i + 1)), e);
-}
-
-// reduce (used when the filter finish did not build the smoother chunk
-// elements, e.g. a sharded smoother-reduce call): suffix element
-// a_{k0} (x) ... (x) a_{k1-1} of the chunk, built backwards
-template <typename S, int NX>
-__global__ void __launch_bounds__(kStageNT)
-    k_smoother_reduce(ModelView<S> m, const S* fmean, const S* fcov, long long L,
-                      long long nchunks, S* agg, long long cap, int pf, unsigned* err) {
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  unsigned e = 0;
-  const long long k0 = c * L;
-  const long long k1 = min(k0 + L, m.t);
-  SElem<S, NX> a;
-  for (long long i = k1 - 1; i >= k0; --i) {
-    if (i > k0) prefetch_smoother_in<S, NX>(m, fmean, fcov, i - 1, pf);
-    Vec<S, NX> x;
-    Mat<S, NX, NX> P;
-    load_state(fmean, fcov, i, x, P);
-    const SElem<S, NX> ei = smoother_elem_at<S, NX>(m, i, x, P, e);
-    a = i == k1 - 1 ? ei : smoother_combine(ei, a);
-  }
-  se_store(agg, cap, c, a);
-  if (e) atomicOr(err, e);
-}
-
 // finish: sequential RTS over the chunk from the carried suffix (the
-// inclusive reversed prefix of chunk c+1 = smoothed state at step k1).  In a
-// time-sharded run `carry` holds the smoothed state after the shard (fold of
-// the successor shards' elements, E = 0): the incoming state of chunk
-// c < nchunks-1 is then (local suffix of chunk c+1) (x) carry.
+// inclusive reversed prefix of chunk c+1 = smoothed state at step k1), driven
+// by the per-step smoothing elements of the filter finish:
+// x_s(k) = E_k x_s(k+1) + g_k, P_s(k) = E_k P_s(k+1) E_k^T + L_k (Lemma 2
+// with a state on the right).  In a time-sharded run `carry` holds the
+// smoothed state after the shard (fold of the successor shards' elements,
+// E = 0): the incoming state of chunk c < nchunks-1 is then
+// (local suffix of chunk c+1) (x) carry.
 template <typename S, int NX>
-__global__ void __launch_bounds__(kStageNT)
-    k_smoother_finish(ModelView<S> m, long long L, long long nchunks, const S* suf,
-                      long long suf_cap, const S* carry, S* mean, S* cov, int pf,
-                      unsigned* err) {
+__global__ void __launch_bounds__(128)
+    k_smoother_finish(long long t, long long L, long long nchunks, const S* suf,
+                      long long suf_cap, const S* carry, const S* egl, S* mean, S* cov) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
-  unsigned e = 0;
   const long long k0 = c * L;
-  const long long k1 = min(k0 + L, m.t);
-  Vec<S, NX> gs;
-  Mat<S, NX, NX> Ls;
+  const long long k1 = min(k0 + L, t);
+  constexpr int ES = EglLayout<NX>::size;
+  Vec<S, NX> gs = zeros<S, NX, 1>();
+  Mat<S, NX, NX> Ls = zeros<S, NX, NX>();
   if (c + 1 < nchunks) {
     gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + (c + 1), suf_cap);
     Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + (c + 1), suf_cap);
@@ -675,25 +742,15 @@ __global__ void __launch_bounds__(kStageNT)
     gs = load<S, NX, 1>(carry);
     Ls = load<S, NX, NX>(carry + NX);
   }
-  // `mean`/`cov` hold the filtered stats on entry (in place: each step is
-  // read before the same thread overwrites it)
+  // the series' last step has E = 0 (terminal element), so the zero state
+  // entering the last chunk of an unsharded run is never used
   for (long long i = k1 - 1; i >= k0; --i) {
-    if (i > k0) prefetch_smoother_in<S, NX>(m, mean, cov, i - 1, pf);
-    Vec<S, NX> x;
-    Mat<S, NX, NX> P;
-    load_state(mean, cov, i, x, P);
-    if (i == m.last_step) {
-      gs = x;
-      Ls = P;
-    } else {
-      const SElem<S, NX> ei = smoother_elem_at<S, NX>(m, i, x, P, e);
-      gs = mul_add(ei.E, gs, ei.g);
-      const Mat<S, NX, NX> el = mul(ei.E, Ls);
-      Ls = mul_nt_sym_add(el, ei.E, ei.L);
-    }
+    const SElem<S, NX> ei = egl_load<S, NX>(egl + (i - k0) * ES * suf_cap + c, suf_cap);
+    gs = mul_add(ei.E, gs, ei.g);
+    const Mat<S, NX, NX> el = mul(ei.E, Ls);
+    Ls = mul_nt_sym_add(el, ei.E, ei.L);
     store_state(mean, cov, i, gs, Ls);
   }
-  if (e) atomicOr(err, e);
 }
 
 // ============================================================================

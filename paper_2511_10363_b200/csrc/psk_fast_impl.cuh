@@ -8,6 +8,7 @@
 #include "psk_exact.h"
 #include "psk_fast.cuh"
 #include "psk_levels.cuh"
+#include "psk_tma.hpp"
 
 namespace psk {
 
@@ -55,6 +56,7 @@ struct FastScratch {
   ScanPlan plan;
   S *agg = nullptr, *aux1 = nullptr, *aux2 = nullptr;
   S* sagg = nullptr;        // smoother chunk elements (built by the filter finish)
+  S* egl = nullptr;         // per-step smoothing elements (PRTS only)
   bool sagg_valid = false;
   void* dlb = nullptr;
 };
@@ -76,6 +78,13 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
   sc.agg = (S*)alloc(sizeof(S) * FS * (sc.npad ? sc.npad : 1), actx);
   sc.sagg = (S*)alloc(sizeof(S) * SLayout<NX>::size * (sc.npad ? sc.npad : 1), actx);
   sc.sagg_valid = false;
+  sc.egl = nullptr;
+  if (a.method == 1) {
+    sc.egl = (S*)alloc(sizeof(S) * (size_t)EglLayout<NX>::size * (size_t)sc.chunk *
+                           (size_t)(sc.npad ? sc.npad : 1),
+                       actx);
+    if (!sc.egl) return 8;
+  }
   sc.aux1 = (S*)alloc(sizeof(S) * FS * (a1 ? a1 : 1), actx);
   sc.aux2 = (S*)alloc(sizeof(S) * FS * (a2 ? a2 : 1), actx);
   sc.dlb = dlb ? alloc(dlb_state_bytes<S, NX>(sc.nchunks), actx) : nullptr;
@@ -106,11 +115,20 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
     }
   };
   const int gs = blocks_for(nch, kStageNT);
-  const int pf = a.prefetch;
+  // TMA stage of the per-step inputs (psk_stage.cuh): two stages of the CTA
+  const int stage_bytes = FilterTma<S, NX, NY>::smem;
+  const long long nfull = m.t / Lc;  // complete chunks (extent of the tensor maps)
+  StageMaps maps;
+  if (phase == 0 || phase == 1) {
+    const int st = make_stage_maps<S, NX, NY>(m, Lc, nfull, maps);
+    if (st) return st;
+  }
   switch (phase) {
     case 0:
-      k_filter_reduce<S, NX, NY><<<gs, kStageNT, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, pf,
-                                                                L.err);
+      cudaFuncSetAttribute(k_filter_reduce<S, NX, NY>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+      k_filter_reduce<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
+          m, maps, Lc, nch, nfull, sc.agg, npad, L.err);
       L.count("filter_reduce");
       fill(fops, sc.agg);
       chunk_scan(L, fops, a, sc.agg, nch, npad, 0, sc.aux1, sc.aux2, sc.plan, sc.dlb);
@@ -120,18 +138,18 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       }
       break;
     case 1:  // filter finish; for PRTS also folds the smoother chunk elements
-      k_filter_finish<S, NX, NY><<<gs, kStageNT, 0, L.stream>>>(
-          m, Lc, nch, sc.agg, npad, carry, mean, cov, a.method == 1 ? sc.sagg : nullptr, npad,
-          pf, L.err);
+      cudaFuncSetAttribute(k_filter_finish<S, NX, NY>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+      k_filter_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
+          m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov,
+          a.method == 1 ? sc.sagg : nullptr, npad, a.method == 1 ? sc.egl : nullptr, L.err);
       L.count(a.method == 1 ? "filter_finish_smoother_reduce" : "filter_finish");
       sc.sagg_valid = a.method == 1;
       break;
     case 2:
-      if (!sc.sagg_valid) {
-        k_smoother_reduce<S, NX><<<gs, kStageNT, 0, L.stream>>>(m, mean, cov, Lc, nch,
-                                                                sc.sagg, npad, pf, L.err);
-        L.count("smoother_reduce");
-      }
+      // the smoother chunk elements and per-step elements come from the
+      // PRTS filter finish (phase 1)
+      if (!sc.sagg_valid || sc.egl == nullptr) return 7;
       fill(sops, sc.sagg);
       chunk_scan(L, sops, a, sc.sagg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
       if (elem_out) {
@@ -140,8 +158,9 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       }
       break;
     case 3:
-      k_smoother_finish<S, NX><<<gs, kStageNT, 0, L.stream>>>(m, Lc, nch, sc.sagg, npad,
-                                                              carry, mean, cov, pf, L.err);
+      if (sc.egl == nullptr) return 7;
+      k_smoother_finish<S, NX><<<blocks_for(nch, 128), 128, 0, L.stream>>>(
+          m.t, Lc, nch, sc.sagg, npad, carry, sc.egl, mean, cov);
       L.count("smoother_finish");
       sc.sagg_valid = false;
       break;
@@ -169,14 +188,12 @@ static int fast_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, 
   FastScratch<S> sc;
   int st = fast_prepare_t<S, NX>(m, a, sc, alloc, actx);
   if (st) return st;
-  fast_phase_t<S, NX, NY>(L, m, a, sc, 0, mean, cov, nullptr, nullptr);
-  fast_phase_t<S, NX, NY>(L, m, a, sc, 1, mean, cov, nullptr, nullptr);
-  if (a.method == 1) {
-    fast_phase_t<S, NX, NY>(L, m, a, sc, 2, mean, cov, nullptr, nullptr);
-    fast_phase_t<S, NX, NY>(L, m, a, sc, 3, mean, cov, nullptr, nullptr);
-  } else if (a.method == 2) {
-    fast_phase_t<S, NX, NY>(L, m, a, sc, 4, mean, cov, nullptr, nullptr);
-    fast_phase_t<S, NX, NY>(L, m, a, sc, 5, mean, cov, nullptr, nullptr);
+  const int phases[2][4] = {{0, 1, 2, 3}, {0, 1, 4, 5}};
+  const int n = a.method == 0 ? 2 : 4;
+  for (int i = 0; i < n; ++i) {
+    st = fast_phase_t<S, NX, NY>(L, m, a, sc, phases[a.method == 2][i], mean, cov, nullptr,
+                                 nullptr);
+    if (st) return st;
   }
   return 0;
 }

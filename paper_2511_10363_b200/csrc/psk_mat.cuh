@@ -31,10 +31,41 @@ template <typename S>
 __device__ __forceinline__ S sabs(S x) {
   return x < S(0) ? -x : x;
 }
-__device__ __forceinline__ double srcp(double x) { return 1.0 / x; }
-__device__ __forceinline__ float srcp(float x) { return 1.0f / x; }
+// Branch-free reciprocal and reciprocal square root: the MUFU approximation
+// refined by Newton steps (quadratic convergence; two steps take the FP64
+// seed below 1 ulp).  IEEE `1.0 / x` and `sqrt(x)` compile to a fast path
+// plus a slow-path branch each, which splits every per-step body into many
+// basic blocks and stops the scheduler from overlapping the independent
+// filter / smoother-element / fold dependency chains (profiles/r01_v2).
+// correctly rounded square root (exact mode: bitwise with the reference)
 __device__ __forceinline__ double ssqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float ssqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double srcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float srcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+__device__ __forceinline__ double srsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  r = fma(r, fma(-h * r, r, 0.5), r);
+  return fma(r, fma(-h * r, r, 0.5), r);
+}
+__device__ __forceinline__ float srsqrt(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  const float h = 0.5f * x;
+  return fmaf(r, fmaf(-h * r, r, 0.5f), r);
+}
 __device__ __forceinline__ double sfma(double a, double b, double c) {
   return fma(a, b, c);
 }
@@ -374,8 +405,8 @@ __device__ __forceinline__ Chol<S, N> cholesky(const Mat<S, N, N>& a,
 #pragma unroll
     for (int k = 0; k < j; ++k) diag = sfma(-c.l.a[j][k], c.l.a[j][k], diag);
     if (!(diag > S(0))) err |= kErrNotPD;
-    S ljj = ssqrt(diag);
-    S il = srcp(ljj);
+    const S il = srsqrt(diag);  // 1 / l(j,j)
+    const S ljj = diag * il;
     c.l.a[j][j] = ljj;
     c.inv[j] = il;
 #pragma unroll

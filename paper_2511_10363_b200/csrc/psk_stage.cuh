@@ -1,16 +1,22 @@
-// psk_stage.cuh -- per-thread asynchronous staging of per-step model blocks
-// into shared memory (cp.async, LDGSTS), double-buffered.
+// psk_stage.cuh -- TMA staging of the per-step model blocks into shared
+// memory (cp.async.bulk.tensor + mbarrier), double-buffered.
 //
-// Every fast-path thread walks its own chunk of consecutive steps, so the
-// natural access is "one thread, one contiguous 16..128-byte block per field
-// per step".  Issuing the loads for step k+1 before computing step k keeps
-// enough bytes in flight to saturate HBM without spending registers (the
-// per-step model is 52 scalars = 416 B at nx=4, ny=2, f64).  The shared layout
-// is granule-major: granule g of a field for thread t lives at
-// base + g * U * NT + t * U (U = 16/8/4 bytes), so a warp's 16-byte reads are
-// bank-conflict-free and each thread only ever touches its own granules (no
-// block-level barrier is needed -- cp.async.wait_group is per thread).
+// Every fast-path thread walks its own chunk of L consecutive steps; a CTA of
+// kStageNT threads owns kStageNT consecutive chunks, so at walk position j it
+// needs step j of each of them: kStageNT blocks spaced L steps apart in every
+// field array.  Viewed as a 3-D tensor [row, L, chunks] (row = one step's
+// block, padded to 16 bytes), that set is ONE tensor-map box {row, 1,
+// kStageNT} per field -- seven TMA instructions fetch a whole step of the
+// CTA.  Measured on the pure chunk walk (psk_membench.cu, profiles/r01_v2):
+// TMA boxes 6.4-7.1 TB/s against 3.5-4.0 TB/s for warp-cooperative LDGSTS,
+// 1.5-1.9 TB/s for per-thread loads and 2.2 TB/s for per-thread bulk copies.
+//
+// Box rows are swizzled by the TMA unit (128/64/32-byte modes for 128/64/
+// 32-byte rows) so that each thread's 16-byte reads of its own row are
+// bank-conflict-free; rows of other widths are unswizzled (odd multiples of
+// 16 bytes are conflict-free as they are).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -19,103 +25,116 @@
 
 namespace psk {
 
-template <int BYTES>
-struct Gran {
-  static constexpr int U = BYTES % 16 == 0 ? 16 : (BYTES % 8 == 0 ? 8 : 4);
-  static constexpr int N = BYTES / U;
-};
+constexpr int kStageNT = 128;  // threads (= chunks) per CTA of a staged walk
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-template <int U>
-__device__ __forceinline__ void cp_async(void* dst, const void* src) {
-  if constexpr (U == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-  else if constexpr (U == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "PSK_WAIT: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PSK_WAIT;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
+      : "memory");
 }
 
-// A field of BYTES bytes per thread per step at byte offset OFF (per stage)
+// One staged field: BYTES per step, row = BYTES rounded up to 16, box of
+// kStageNT rows at byte OFF (1024-aligned) of a stage.
 template <int OFF, int BYTES>
-struct Field {
-  static constexpr int off = OFF, bytes = BYTES;
-  static constexpr int U = Gran<BYTES>::U, N = Gran<BYTES>::N;
+struct TField {
+  static constexpr int bytes = BYTES;
+  static constexpr int row = (BYTES + 15) / 16 * 16;
+  static constexpr int swz = row == 128 ? 3 : (row == 64 ? 2 : (row == 32 ? 1 : 0));
+  static constexpr int off = OFF;
+  static constexpr int end = OFF + (row * kStageNT + 1023) / 1024 * 1024;
 };
-
-// Stage buffer of NT threads: `base` points at this stage's shared bytes.
-template <int NT>
-struct Stage {
-  unsigned char* base;
-  template <class F>
-  __device__ __forceinline__ void fetch(const void* src) const {
-    const unsigned char* s = static_cast<const unsigned char*>(src);
+// byte offset of 16-byte chunk c of row r inside the field's box (the TMA
+// swizzle: address bits [4, 4+swz) ^= bits [7, 7+swz))
+template <class F>
+__device__ __forceinline__ int tma_off(int r, int c) {
+  const int a = r * F::row + c * 16;
+  return a ^ (((a >> 7) & ((1 << F::swz) - 1)) << 4);
+}
+// this thread's block of a staged field as a row-major R x C matrix
+template <class F, typename S, int R, int C>
+__device__ __forceinline__ Mat<S, R, C> tma_get(const unsigned char* stage, int t) {
+  static_assert(R * C * (int)sizeof(S) == F::bytes, "field size");
+  Mat<S, R, C> m;
+  S* o = &m.a[0][0];
+  constexpr int per = 16 / sizeof(S);
+  constexpr int n = R * C;
 #pragma unroll
-    for (int g = 0; g < F::N; ++g)
-      cp_async<F::U>(base + F::off * NT + g * F::U * NT + threadIdx.x * F::U, s + g * F::U);
-  }
-  template <class F, typename S, int R, int C>
-  __device__ __forceinline__ Mat<S, R, C> get() const {
-    static_assert(R * C * (int)sizeof(S) == F::bytes, "field size");
-    Mat<S, R, C> m;
-    S* o = &m.a[0][0];
+  for (int c = 0; c < (n + per - 1) / per; ++c) {
+    const unsigned char* p = stage + F::off + tma_off<F>(t, c);
+    if ((c + 1) * per <= n) {
+      const float4 v = *reinterpret_cast<const float4*>(p);
+      const S* vs = reinterpret_cast<const S*>(&v);
 #pragma unroll
-    for (int g = 0; g < F::N; ++g) {
-      const unsigned char* p = base + F::off * NT + g * F::U * NT + threadIdx.x * F::U;
-      if constexpr (F::U == 16) {
-        const float4 v = *reinterpret_cast<const float4*>(p);
-        const S* vs = reinterpret_cast<const S*>(&v);
+      for (int j = 0; j < per; ++j) o[c * per + j] = vs[j];
+    } else {
 #pragma unroll
-        for (int j = 0; j < 16 / (int)sizeof(S); ++j) o[g * (16 / sizeof(S)) + j] = vs[j];
-      } else if constexpr (F::U == 8) {
-        const float2 v = *reinterpret_cast<const float2*>(p);
-        const S* vs = reinterpret_cast<const S*>(&v);
-#pragma unroll
-        for (int j = 0; j < 8 / (int)sizeof(S); ++j) o[g * (8 / sizeof(S)) + j] = vs[j];
-      } else {
-        o[g] = *reinterpret_cast<const S*>(p);
-      }
+      for (int j = 0; j < per; ++j)
+        if (c * per + j < n) o[c * per + j] = reinterpret_cast<const S*>(p)[j];
     }
-    return m;
   }
+  return m;
+}
+
+// The staged filter inputs (F, u, Q, H, d, R, y) of one step of a CTA
+template <typename S, int NX, int NY>
+struct FilterTma {
+  static constexpr int s = sizeof(S);
+  using F = TField<0, NX * NX * s>;
+  using u = TField<F::end, NX * s>;
+  using Q = TField<u::end, NX * NX * s>;
+  using H = TField<Q::end, NY * NX * s>;
+  using d = TField<H::end, NY * s>;
+  using R = TField<d::end, NY * NY * s>;
+  using y = TField<R::end, NY * s>;
+  static constexpr int stage = y::end;  // bytes of one stage (1024-aligned)
+  __host__ __device__ static constexpr int off(int f) {
+    return f == 0 ? F::off : f == 1 ? u::off : f == 2 ? Q::off : f == 3 ? H::off
+         : f == 4 ? d::off : f == 5 ? R::off : y::off;
+  }
+  __host__ __device__ static constexpr int row(int f) {
+    return f == 0 ? F::row : f == 1 ? u::row : f == 2 ? Q::row : f == 3 ? H::row
+         : f == 4 ? d::row : f == 5 ? R::row : y::row;
+  }
+  // dynamic shared memory of a double-buffered walk (+ alignment slack and
+  // the two mbarriers)
+  static constexpr int smem = 2 * stage + 1024 + 64;
 };
 
-// Per-step filter inputs (F, u, Q, H, d, R, y), byte offsets within a stage
-// (multiplied by NT inside Stage)
-template <typename S, int NX, int NY>
-struct FilterIn {
-  static constexpr int s = sizeof(S);
-  using F = Field<0, NX * NX * s>;
-  using u = Field<F::off + F::bytes, NX * s>;
-  using Q = Field<u::off + u::bytes, NX * NX * s>;
-  using H = Field<Q::off + Q::bytes, NY * NX * s>;
-  using d = Field<H::off + H::bytes, NY * s>;
-  using R = Field<d::off + d::bytes, NY * NY * s>;
-  using y = Field<R::off + R::bytes, NY * s>;
-  static constexpr int bytes = y::off + y::bytes;  // per thread per stage
-};
-// Per-step smoother inputs: filtered (x, P)_i and the transition (F, Q, u)_{i+1}
-template <typename S, int NX>
-struct SmootherIn {
-  static constexpr int s = sizeof(S);
-  using x = Field<0, NX * s>;
-  using P = Field<x::off + x::bytes, NX * NX * s>;
-  using F = Field<P::off + P::bytes, NX * NX * s>;
-  using Q = Field<F::off + F::bytes, NX * NX * s>;
-  using u = Field<Q::off + Q::bytes, NX * s>;
-  static constexpr int bytes = u::off + u::bytes;
+// Tensor maps of the seven model fields for one staged launch (kernel
+// parameter; `use[f]` = 0 for a broadcast field, read straight from global).
+struct StageMaps {
+  CUtensorMap m[7];
+  int use[7];
+  unsigned tx;  // bytes one stage receives (sum of the used boxes)
 };
 
 }  // namespace psk

@@ -1,0 +1,67 @@
+// psk_tma.hpp -- host side of the TMA stage (psk_stage.cuh): one 3-D tensor
+// map per model field, [row, L, nfull] = (one step's block padded to a 16-byte
+// row) x (steps of a chunk) x (complete chunks), box {row, 1, kStageNT}.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+#include "psk_common.cuh"
+#include "psk_stage.cuh"
+
+namespace psk {
+
+inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Fill `maps` for a staged walk over chunks of L steps, `nfull` of them
+// complete.  Returns 0, or 9 when a non-broadcast field cannot be described
+// (prepare_model packs every field into a TMA-compatible pitch, so this
+// signals a bug rather than a user error).
+template <typename S, int NX, int NY>
+int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMaps& maps) {
+  using In = FilterTma<S, NX, NY>;
+  const S* base[7] = {m.f, m.u, m.q, m.h, m.d, m.r, m.y};
+  const long long stride[7] = {m.sf, m.su, m.sq, m.sh, m.sd, m.sr, m.sy};
+  maps.tx = 0;
+  for (int f = 0; f < 7; ++f) {
+    maps.use[f] = 0;
+    if (stride[f] == 0 || nfull <= 0) continue;  // broadcast: read from global
+    auto enc = tma_encoder();
+    const int row = In::row(f);
+    const unsigned long long pitch = (unsigned long long)stride[f] * sizeof(S);
+    if (!enc || reinterpret_cast<uintptr_t>(base[f]) % 16 || pitch % 16 || pitch < (unsigned)row)
+      return 9;
+    cuuint64_t dims[3] = {(cuuint64_t)(row / sizeof(S)), (cuuint64_t)L, (cuuint64_t)nfull};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * (cuuint64_t)L};
+    cuuint32_t box[3] = {(cuuint32_t)(row / sizeof(S)), 1, (cuuint32_t)kStageNT};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapSwizzle sw = row == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : row == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUresult r =
+        enc(&maps.m[f],
+            sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+            3, const_cast<S*>(base[f]), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 9;
+    maps.use[f] = 1;
+    maps.tx += (unsigned)(row * kStageNT);
+  }
+  return 0;
+}
+
+}  // namespace psk
