@@ -189,7 +189,7 @@ def main() -> None:
     ap.add_argument("--impl", default="psk", choices=["psk", "reference"])
     ap.add_argument("--log2t", type=int, default=24)
     ap.add_argument("--alg", default="DecoupledLookback")
-    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--chunk", type=int, default=0, help="steps per chunk, 0 = auto (one wave)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--broadcast", action="store_true")
     ap.add_argument("--ref-log2t", type=int, default=18)

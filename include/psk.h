@@ -62,7 +62,9 @@ typedef enum { PSK_HOST = 0, PSK_DEVICE = 1 } psk_space;
  *  PSK_MODE_FAST  (default): chunked kernels -- each thread folds `chunk`
  *      consecutive steps into a scan element, the chunk elements are scanned
  *      with the selected ScanAlg, and a per-chunk pass writes the outputs.
- *      chunk = 1 is the paper's one-element-per-step formulation.
+ *      chunk = 1 is the paper's one-element-per-step formulation; chunk = 0
+ *      (default) picks the chunk length per call so that the chunks exactly
+ *      fill "waves" waves of co-resident threads.
  *  PSK_MODE_EXACT: the reference's level-by-level scan kernels
  *      (scan.hpp:198-444) with the reference's operation order and no FMA
  *      contraction -- bitwise equal to the reference CPU path. */
@@ -93,11 +95,13 @@ typedef struct psk_ctx psk_ctx;
  * with PSK_E_CUDA when no device is present). */
 int psk_create(psk_ctx** ctx, int device);
 int psk_destroy(psk_ctx* ctx);
-/* Mode and tuning: mode (psk_mode), chunk length (>= 1) */
+/* Mode and tuning: mode (psk_mode), chunk length (>= 1, or 0 = auto) */
 int psk_set_mode(psk_ctx* ctx, int mode);
 int psk_set_chunk(psk_ctx* ctx, int chunk);
 /* Named tuning options of the fast path:
- *   "chunk"     steps folded per thread (same as psk_set_chunk)
+ *   "chunk"     steps folded per thread, 0 = auto (same as psk_set_chunk)
+ *   "waves"     auto chunk: the chunks fill this many waves of co-resident
+ *               threads (default 4)
  * Returns PSK_E_ARG for an unknown key or value. */
 int psk_set_option(psk_ctx* ctx, const char* key, int64_t value);
 /* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).

@@ -158,7 +158,7 @@ class CudaBackend:
     reference's ``PoolBackend`` it must not be driven by two callers at once.
     """
 
-    def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 64,
+    def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 0,
                  stream: Any = None) -> None:
         L = _lib.lib()
         ctx = C.c_void_p()

@@ -36,7 +36,8 @@ struct psk_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int mode = PSK_MODE_FAST;
-  long long chunk = 64;
+  long long chunk = 0;  // 0: auto (whole waves of chunks)
+  int waves = 4;        // waves of chunks for the auto chunk length
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
@@ -221,6 +222,7 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     a.alg = alg;
     a.sengupta_n = sengupta_n;
     a.chunk = ctx->chunk;
+    a.waves = ctx->waves;
     st = fast_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
     if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
     if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
@@ -306,6 +308,7 @@ int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   a.alg = alg;
   a.sengupta_n = sn;
   a.chunk = ctx->chunk;
+  a.waves = ctx->waves;
   if (phase != 0 && phase != 2) {  // finishes reuse the scan spec of the reduce
     a.alg = ctx->shard_alg;
     a.sengupta_n = ctx->shard_sn;
@@ -469,7 +472,7 @@ int psk_set_mode(psk_ctx* c, int mode) {
 
 int psk_set_chunk(psk_ctx* c, int chunk) {
   if (!c) return fail(PSK_E_ARG, "null context");
-  if (chunk < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
+  if (chunk < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
   c->chunk = chunk;
   return PSK_OK;
 }
@@ -478,8 +481,11 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(PSK_E_ARG, "null context or key");
   const std::string k(key);
   if (k == "chunk") {
-    if (value < 1) return fail(PSK_E_ARG, "chunk must be >= 1");
+    if (value < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
     c->chunk = value;
+  } else if (k == "waves") {
+    if (value < 1 || value > 1024) return fail(PSK_E_ARG, "waves must be 1..1024");
+    c->waves = (int)value;
   } else {
     return fail(PSK_E_ARG, "unknown option " + k);
   }

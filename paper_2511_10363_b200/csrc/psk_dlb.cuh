@@ -28,6 +28,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "psk_common.cuh"
 #include "psk_exact.h"
 
@@ -38,6 +42,16 @@ constexpr int kDlbLevels = 7;  // log2(kDlbThreads)
 static_assert((1 << kDlbLevels) == kDlbThreads, "CTA must be 2^kDlbLevels threads");
 constexpr int kDlbSlots = kDlbThreads + 2;  // + exclusive tile prefix + scratch
 
+// Optional phase trace (tools/dlb_trace.py): thread 0 of every tile stamps
+// %globaltimer at the phase boundaries into trace[tile * 8 + i].
+__device__ __forceinline__ void dlb_stamp(unsigned long long* trace, long long tile, int i) {
+  if (trace != nullptr && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    trace[tile * 8 + i] = g;
+  }
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -47,27 +61,30 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// elements per thread: the smallest K >= 1 that keeps the tile count within
-// about one resident wave (148 SMs x 3 CTAs), capped at 16
-inline int dlb_per_thread(long long n) {
-  const long long target = 148LL * 3 * kDlbThreads;
+// Elements per thread: the smallest K >= 1 that keeps every tile resident in
+// ONE wave (`resident` = co-resident CTAs of k_dlb on the device, from the
+// occupancy calculator), so the look-back never waits on a tile that has not
+// started and spans at most ceil(resident / 128) windows.
+inline int dlb_per_thread(long long n, long long resident) {
+  const long long target = (resident > 0 ? resident : 148) * kDlbThreads;
   long long k = (n + target - 1) / target;
   if (k < 1) k = 1;
-  if (k > 16) k = 16;
+  if (k > 64) k = 64;
   return (int)k;
 }
-inline long long dlb_tiles(long long n) {
-  const long long per = (long long)kDlbThreads * dlb_per_thread(n);
-  return (n + per - 1) / per;
+inline long long dlb_tiles(long long n, int per) {
+  const long long tile = (long long)kDlbThreads * per;
+  return (n + tile - 1) / tile;
 }
 __host__ __device__ inline size_t dlb_head_bytes(long long ntiles) {
   return 256 + ((size_t)ntiles * 4 + 255) / 256 * 256;
 }
 // state layout: [ticket u32 | pad][flags u32 x ntiles][agg FS x ntiles]
 //               [incl FS x ntiles][thread prefixes FS x ntiles*kDlbThreads]
+// sized for the worst case K = 1 (one element per thread)
 template <typename S, int NX>
 inline size_t dlb_state_bytes(long long n) {
-  const long long nt = dlb_tiles(n);
+  const long long nt = dlb_tiles(n, 1);
   const size_t fs = (size_t)(3 * NX * NX + 2 * NX);
   return dlb_head_bytes(nt) + sizeof(S) * fs * (size_t)nt * (2 + kDlbThreads);
 }
@@ -75,7 +92,7 @@ inline size_t dlb_state_bytes(long long n) {
 template <class Ops>
 __global__ void __launch_bounds__(kDlbThreads)
     k_dlb(Ops ops, typename Ops::S* buf, long long n, int rev, char* state,
-          long long ntiles, int per) {
+          long long ntiles, int per, unsigned long long* trace) {
   using S = typename Ops::S;
   extern __shared__ __align__(16) unsigned char dlb_smem[];
   S* sm = reinterpret_cast<S*>(dlb_smem);
@@ -97,6 +114,7 @@ __global__ void __launch_bounds__(kDlbThreads)
   if (t == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const long long tile = s_tile;
+  dlb_stamp(trace, tile, 0);
   // logical (x) on (buffer, index) pairs: reversed scans flip the operands
   auto lcomb = [&](const ElemBuf<S>& d, long long di, const ElemBuf<S>& l, long long li,
                    const ElemBuf<S>& r, long long ri) {
@@ -117,6 +135,7 @@ __global__ void __launch_bounds__(kDlbThreads)
     ops.identity(sb, t);
   }
   __syncthreads();
+  dlb_stamp(trace, tile, 1);
   // 3. tile scan of the thread aggregates: up-sweep, then Ladner-Fischer down
 #pragma unroll 1
   for (int d = 0; d < kDlbLevels; ++d) {
@@ -136,6 +155,7 @@ __global__ void __launch_bounds__(kDlbThreads)
     }
     __syncthreads();
   }
+  dlb_stamp(trace, tile, 2);
   // 4. publish the tile aggregate (tile 0: its inclusive prefix); park the
   // thread-inclusive prefixes in global scratch (the slots become the window)
   constexpr int last = kDlbThreads - 1;
@@ -193,6 +213,7 @@ __global__ void __launch_bounds__(kDlbThreads)
       if (stop < kDlbThreads || base - kDlbThreads < 0) break;
       base -= kDlbThreads;
     }
+    dlb_stamp(trace, tile, 3);
     // 6. publish the inclusive prefix of the tile
     if (t == 0) {
       lcomb(sb, kTmp, sb, kExcl, sb, kTmp);
@@ -202,6 +223,7 @@ __global__ void __launch_bounds__(kDlbThreads)
     }
     __syncthreads();
   }
+  dlb_stamp(trace, tile, 4);
   // thread-exclusive prefix: (tile exclusive) (x) (thread-inclusive of t-1)
   if (tile == 0) {
     // shift slot t-1 -> t through registers (all reads before all writes)
@@ -239,6 +261,8 @@ __global__ void __launch_bounds__(kDlbThreads)
       }
     }
   }
+  __syncthreads();
+  dlb_stamp(trace, tile, 5);
 }
 
 template <class Ops>
@@ -246,14 +270,37 @@ void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf,
               long long n, int rev, typename Ops::S* /*unused*/, void* state) {
   using S = typename Ops::S;
   if (n <= 0) return;
-  const int per = dlb_per_thread(n);
-  const long long ntiles = dlb_tiles(n);
-  cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
   const size_t smem = sizeof(S) * (size_t)Ops::kSize * kDlbSlots;
   // the attribute is per device: set it on every call (cheap)
   cudaFuncSetAttribute(k_dlb<Ops>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dlb<Ops>, kDlbThreads, smem);
+  const int per = dlb_per_thread(n, (long long)sms * per_sm);
+  const long long ntiles = dlb_tiles(n, per);
+  cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
+  static unsigned long long* trace = nullptr;  // PSK_DLB_TRACE: stamps of the last scan
+  static long long trace_tiles = 0;
+  if (std::getenv("PSK_DLB_TRACE") != nullptr) {
+    if (trace == nullptr) cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 65536);
+    trace_tiles = ntiles;
+  }
   k_dlb<Ops><<<(unsigned)ntiles, kDlbThreads, smem, L.stream>>>(
-      ops, buf, n, rev, reinterpret_cast<char*>(state), ntiles, per);
+      ops, buf, n, rev, reinterpret_cast<char*>(state), ntiles, per,
+      trace != nullptr && ntiles <= 65536 ? trace : nullptr);
+  if (trace != nullptr && std::getenv("PSK_DLB_TRACE") != nullptr) {
+    std::vector<unsigned long long> h((size_t)trace_tiles * 8);
+    cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, L.stream);
+    cudaStreamSynchronize(L.stream);
+    FILE* f = std::fopen(std::getenv("PSK_DLB_TRACE"), "ab");
+    if (f) {
+      const long long hdr[4] = {ntiles, per, (long long)Ops::kSize, n};
+      std::fwrite(hdr, sizeof(hdr), 1, f);
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   L.count("chunk_scan_dlb");
 }
 

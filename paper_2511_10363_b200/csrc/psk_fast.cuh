@@ -648,20 +648,51 @@ __device__ __forceinline__ void filter_incoming(const ModelView<S>& m, long long
   }
 }
 
+// Smoothing element of step k-1 from its filtered (x, P) and the prediction
+// to step k that the filter computes anyway (kalman_elems.hpp:151-193 with
+// FP = F P, PP = F P F^T + Q and F x + u shared with kf_predict):
+// E^T = PP^-1 FP (Cholesky), g = x - E (F x + u), L = P - E FP (symmetric).
+template <typename S, int NX>
+__device__ __forceinline__ SElem<S, NX> smoother_elem_pred(const Vec<S, NX>& x,
+                                                           const Mat<S, NX, NX>& P,
+                                                           const Mat<S, NX, NX>& fp,
+                                                           const Mat<S, NX, NX>& pp,
+                                                           const Vec<S, NX>& xp, unsigned& err) {
+  SElem<S, NX> e;
+  const Chol<S, NX> ch = cholesky(pp, err);
+  const Mat<S, NX, NX> et = chol_solve(ch, fp);  // E^T
+  e.E = trans(et);
+  e.g = sub_mul(x, e.E, xp);
+#pragma unroll
+  for (int a = 0; a < NX; ++a)
+#pragma unroll
+    for (int b = a; b < NX; ++b) {
+      S acc = P.a[a][b];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) acc = sfma(-et.a[k][a], fp.a[k][b], acc);
+      e.L.a[a][b] = acc;
+      e.L.a[b][a] = acc;
+    }
+  return e;
+}
+
 // finish: sequential Kalman filter over the chunk from the carried prefix.
-// PKF/PTFS (egl == nullptr): writes the filtered stats.  PRTS (egl non-null):
-// the filtered stats are not needed by the caller, only the smoother is --
-// the pass writes the per-step smoothing elements e_k (kalman_elems.hpp:
-// 151-193) instead, and folds the chunk's smoothing element e_{k0} (x) ... (x)
-// e_{k1-1} into `sagg` (Lemma 2 is associative, so the chunk element is built
-// forwards).  e_{k-1} needs the filtered state of step k-1 and the
-// transition (F, Q, u)_k that the filter loads for step k anyway.
-template <typename S, int NX, int NY>
+// SMOOTH = false (PKF, PTFS): writes the filtered stats.  SMOOTH = true
+// (PRTS): the caller needs the smoothed stats only, so the pass writes the
+// per-step smoothing elements e_k instead and folds the chunk's smoothing
+// element e_{k0} (x) ... (x) e_{k1-1} into `sagg` (Lemma 2 is associative,
+// so the chunk element is built forwards).  e_{k-1} needs the filtered state
+// of step k-1 and the prediction to step k, which the filter computes for
+// step k anyway.  The step body is branch-free (one basic block: the
+// scheduler overlaps the filter, smoothing-element and fold chains); at the
+// first step of a chunk the element computed from the incoming state belongs
+// to the previous chunk and is replaced by the identity.
+template <typename S, int NX, int NY, bool SMOOTH>
 __global__ void __launch_bounds__(kStageNT, 2)
     k_filter_finish(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
                     long long nchunks, long long nfull, const S* pre, long long pre_cap,
                     const S* carry, S* mean, S* cov, S* sagg, long long scap, S* egl,
-                    unsigned* err) {
+                    long long ecap, unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = c < nchunks;  // idle threads stay for the block barriers
@@ -673,32 +704,49 @@ __global__ void __launch_bounds__(kStageNT, 2)
   Vec<S, NX> x = zeros<S, NX, 1>();
   Mat<S, NX, NX> P = zeros<S, NX, NX>();
   if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
-  SElem<S, NX> sa;
+  SElem<S, NX> sa = se_identity<S, NX>();
   staged_walk<S, NX, NY>(fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
     const Mat<S, NX, NX> F = in.F();
-    const Mat<S, NX, NX> Q = in.Q();
-    const Vec<S, NX> u = in.u();
-    if (egl != nullptr && k > k0) {  // (x, P) still hold the filtered step k-1
-      const SElem<S, NX> ek = smoother_elem(x, P, F, Q, u, e);
-      egl_store(egl + (k - 1 - k0) * ES * scap + c, scap, ek);
-      sa = k - 1 == k0 ? ek : smoother_combine(sa, ek);
-    }
-    x = mul_add(F, x, u);
+    const Vec<S, NX> xp = mul_add(F, x, in.u());
     const Mat<S, NX, NX> fp = mul(F, P);
-    P = mul_nt_sym_add(fp, F, Q);
+    const Mat<S, NX, NX> pp = mul_nt_sym_add(fp, F, in.Q());
+    if constexpr (SMOOTH) {
+      // (x, P) still hold the filtered step k-1
+      unsigned es = 0;
+      const SElem<S, NX> ek = smoother_elem_pred(x, P, fp, pp, xp, es);
+      const bool keep = k > k0;
+      e |= keep ? es : 0u;
+      const SElem<S, NX> id = se_identity<S, NX>();
+      SElem<S, NX> eu;
+#pragma unroll
+      for (int i = 0; i < NX; ++i) {
+        eu.g.a[i][0] = keep ? ek.g.a[i][0] : id.g.a[i][0];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+          eu.E.a[i][j] = keep ? ek.E.a[i][j] : id.E.a[i][j];
+          eu.L.a[i][j] = keep ? ek.L.a[i][j] : id.L.a[i][j];
+        }
+      }
+      sa = smoother_combine(sa, eu);
+      if (keep) egl_store(egl + (k - 1 - k0) * ES * ecap + c, ecap, ek);
+    }
+    x = xp;
+    P = pp;
     kf_update(x, P, in.meas(), e);
-    if (egl == nullptr) store_state(mean, cov, k, x, P);
+    if constexpr (!SMOOTH) store_state(mean, cov, k, x, P);
   });
-  if (live && egl != nullptr) {  // element of the chunk's last step
-    SElem<S, NX> ek;
-    if (k1 - 1 == m.last_step)
-      ek = terminal_elem(x, P);
-    else
-      ek = smoother_elem(x, P, load<S, NX, NX>(m.F(k1)), load<S, NX, NX>(m.Q(k1)),
-                         load<S, NX, 1>(m.U(k1)), e);
-    egl_store(egl + (k1 - 1 - k0) * ES * scap + c, scap, ek);
-    sa = k1 - 1 == k0 ? ek : smoother_combine(sa, ek);
-    se_store(sagg, scap, c, sa);
+  if constexpr (SMOOTH) {
+    if (live) {  // element of the chunk's last step
+      SElem<S, NX> ek;
+      if (k1 - 1 == m.last_step)
+        ek = terminal_elem(x, P);
+      else
+        ek = smoother_elem(x, P, load<S, NX, NX>(m.F(k1)), load<S, NX, NX>(m.Q(k1)),
+                           load<S, NX, 1>(m.U(k1)), e);
+      egl_store(egl + (k1 - 1 - k0) * ES * ecap + c, ecap, ek);
+      sa = smoother_combine(sa, ek);
+      se_store(sagg, scap, c, sa);
+    }
   }
   if (e) atomicOr(err, e);
 }
@@ -715,18 +763,42 @@ __global__ void __launch_bounds__(kStageNT, 2)
 // smoothed state after the shard (fold of the successor shards' elements,
 // E = 0): the incoming state of chunk c < nchunks-1 is then
 // (local suffix of chunk c+1) (x) carry.
+//
+// Each warp walks its 32 chunks backwards in lock-step: the elements of step
+// j-1 arrive by TMA while step j is computed, and the smoothed rows of step j
+// leave by TMA store (SmoothTma, psk_stage.cuh); rows the tensor maps do not
+// cover (the ragged tail chunk, rows that are not whole 16-byte units) are
+// stored directly.
+constexpr int kSmoothNT = 64;  // 2 warps per CTA
+
 template <typename S, int NX>
-__global__ void __launch_bounds__(128)
-    k_smoother_finish(long long t, long long L, long long nchunks, const S* suf,
-                      long long suf_cap, const S* carry, const S* egl, S* mean, S* cov) {
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
+__global__ void __launch_bounds__(kSmoothNT)
+    k_smoother_finish(long long t, long long L, long long nchunks, long long nfull,
+                      const S* suf, long long suf_cap, const S* carry,
+                      const __grid_constant__ SmoothMaps maps, long long ecap, S* mean, S* cov) {
+  using Tm = SmoothTma<S, NX>;
+  constexpr int ES = Tm::ES;
+  extern __shared__ __align__(1024) unsigned char ssm_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      ((reinterpret_cast<uintptr_t>(ssm_raw) + 1023) & ~uintptr_t(1023)) + (size_t)w * Tm::warp);
+  unsigned char* egl_st = sm;                                   // 2 x egl_stage
+  unsigned char* mean_st = sm + 2 * Tm::egl_stage;              // 2 x mean_stage
+  unsigned char* cov_st = mean_st + 2 * Tm::mean_stage;         // 2 x cov_stage
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cov_st + 2 * Tm::cov_stage);
+  const long long cw0 = (long long)blockIdx.x * kSmoothNT + w * 32;  // first chunk of the warp
+  if (cw0 >= nchunks) return;  // warp-uniform (no block barriers below)
+  const long long c = cw0 + lane;
+  const bool live = c < nchunks;
   const long long k0 = c * L;
   const long long k1 = min(k0 + L, t);
-  constexpr int ES = EglLayout<NX>::size;
+  const long long jn = min(L, t - cw0 * L);  // warp-uniform walk length
+  const bool tstore = maps.store && cw0 < nfull;
+  const bool direct_out = !tstore || c >= nfull;
+
   Vec<S, NX> gs = zeros<S, NX, 1>();
   Mat<S, NX, NX> Ls = zeros<S, NX, NX>();
-  if (c + 1 < nchunks) {
+  if (live && c + 1 < nchunks) {
     gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + (c + 1), suf_cap);
     Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + (c + 1), suf_cap);
     if (carry != nullptr) {
@@ -738,19 +810,74 @@ __global__ void __launch_bounds__(128)
       const Mat<S, NX, NX> el = mul(E, cl);
       Ls = mul_nt_sym_add(el, E, Ls);
     }
-  } else if (carry != nullptr) {
+  } else if (live && carry != nullptr) {
     gs = load<S, NX, 1>(carry);
     Ls = load<S, NX, NX>(carry + NX);
   }
   // the series' last step has E = 0 (terminal element), so the zero state
   // entering the last chunk of an unsharded run is never used
-  for (long long i = k1 - 1; i >= k0; --i) {
-    const SElem<S, NX> ei = egl_load<S, NX>(egl + (i - k0) * ES * suf_cap + c, suf_cap);
-    gs = mul_add(ei.E, gs, ei.g);
-    const Mat<S, NX, NX> el = mul(ei.E, Ls);
-    Ls = mul_nt_sym_add(el, ei.E, ei.L);
-    store_state(mean, cov, i, gs, Ls);
+  auto issue = [&](int st, long long j) {
+    fence_proxy_async();
+    mbar_expect_tx(&bars[st], (unsigned)Tm::egl_box);
+    tma_load_2d(egl_st + st * Tm::egl_stage, &maps.egl, (int)cw0, (int)(j * ES), &bars[st]);
+  };
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+    issue((int)((jn - 1) & 1), jn - 1);
   }
+  __syncwarp();
+  for (long long j = jn - 1; j >= 0; --j) {
+    const int st = (int)(j & 1);
+    if (lane == 0 && j > 0) issue(st ^ 1, j - 1);
+    mbar_wait(&bars[st], (unsigned)(((jn - 1 - j) >> 1) & 1));
+    const S* el = reinterpret_cast<const S*>(egl_st + st * Tm::egl_stage);
+    const bool act = live && k0 + j < k1;
+    if (act) {
+      SElem<S, NX> ei;
+      using Lo = EglLayout<NX>;
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+#pragma unroll
+        for (int q = 0; q < NX; ++q) ei.E.a[i][q] = el[(Lo::E + i * NX + q) * 32 + lane];
+#pragma unroll
+      for (int i = 0; i < NX; ++i) ei.g.a[i][0] = el[(Lo::g + i) * 32 + lane];
+      int q = Lo::L;
+#pragma unroll
+      for (int i = 0; i < NX; ++i)
+#pragma unroll
+        for (int p = i; p < NX; ++p) {
+          const S v = el[(q++) * 32 + lane];
+          ei.L.a[i][p] = v;
+          ei.L.a[p][i] = v;
+        }
+      gs = mul_add(ei.E, gs, ei.g);
+      const Mat<S, NX, NX> eL = mul(ei.E, Ls);
+      Ls = mul_nt_sym_add(eL, ei.E, ei.L);
+    }
+    if constexpr (Tm::Mean::bytes % 16 == 0 && Tm::Cov::bytes % 16 == 0) {
+      if (tstore) {
+        // the store issued from this stage two steps ago has left it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        unsigned char* ms = mean_st + st * Tm::mean_stage;
+        unsigned char* cs = cov_st + st * Tm::cov_stage;
+        tma_put<typename Tm::Mean>(ms, lane, gs);
+        tma_put<typename Tm::Cov>(cs, lane, Ls);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&maps.mean, 0, (int)j, (int)cw0, ms);
+          tma_store_3d(&maps.cov, 0, (int)j, (int)cw0, cs);
+          bulk_commit();
+        }
+      }
+    }
+    if (act && direct_out) store_state(mean, cov, k0 + j, gs, Ls);
+    __syncwarp();  // stage st of the elements is refilled next iteration
+  }
+  if (lane == 0) bulk_wait<0>();
 }
 
 // ============================================================================

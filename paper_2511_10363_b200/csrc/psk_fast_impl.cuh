@@ -49,6 +49,29 @@ static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
   }
 }
 
+// Automatic chunk length: the smallest L whose ceil(T / L) chunks fill
+// `waves` waves of co-resident threads of the per-step kernels (whole waves:
+// no tail).  Fewer waves mean fewer chunk elements for the scan (the DLB
+// folds ceil(chunks / resident) per thread), more waves keep the per-step
+// kernels closer to the HBM roof; 4 is the measured optimum at T = 2^24
+// (profiles/r01_v3: L = 64/74/111/148/222/443 -> 5.08/4.96/4.85/4.99/5.03/
+// 5.17 ms per PRTS).
+template <typename S, int NX, int NY>
+long long auto_chunk(long long T, int waves) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int smem = FilterTma<S, NX, NY>::smem;
+  cudaFuncSetAttribute(k_filter_finish<S, NX, NY, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter_finish<S, NX, NY, true>,
+                                                kStageNT, smem);
+  const long long resident = (long long)(sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1) *
+                             kStageNT * (waves > 0 ? waves : 1);
+  const long long L = (T + resident - 1) / resident;
+  return L < 1 ? 1 : L;
+}
+
 // Scratch of one fast run (allocated by fast_prepare).
 template <typename S>
 struct FastScratch {
@@ -57,15 +80,16 @@ struct FastScratch {
   S *agg = nullptr, *aux1 = nullptr, *aux2 = nullptr;
   S* sagg = nullptr;        // smoother chunk elements (built by the filter finish)
   S* egl = nullptr;         // per-step smoothing elements (PRTS only)
+  long long ecap = 0;       // chunk capacity of egl (a multiple of 32: TMA rows)
   bool sagg_valid = false;
   void* dlb = nullptr;
 };
 
-template <typename S, int NX>
+template <typename S, int NX, int NY>
 static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<S>& sc,
                           void* (*alloc)(size_t, void*), void* actx) {
   const long long T = m.t;
-  sc.chunk = a.chunk < 1 ? 1 : a.chunk;
+  sc.chunk = a.chunk >= 1 ? a.chunk : auto_chunk<S, NX, NY>(T, a.waves);
   sc.nchunks = T > 0 ? (T + sc.chunk - 1) / sc.chunk : 0;
   const bool dlb = a.alg == 6;
   sc.npad = (dlb || a.alg == 0) ? sc.nchunks : (long long)next_pow2(sc.nchunks);
@@ -80,8 +104,9 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
   sc.sagg_valid = false;
   sc.egl = nullptr;
   if (a.method == 1) {
+    sc.ecap = (sc.nchunks + 31) / 32 * 32;
     sc.egl = (S*)alloc(sizeof(S) * (size_t)EglLayout<NX>::size * (size_t)sc.chunk *
-                           (size_t)(sc.npad ? sc.npad : 1),
+                           (size_t)(sc.ecap ? sc.ecap : 32),
                        actx);
     if (!sc.egl) return 8;
   }
@@ -138,12 +163,21 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       }
       break;
     case 1:  // filter finish; for PRTS also folds the smoother chunk elements
-      cudaFuncSetAttribute(k_filter_finish<S, NX, NY>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
-      k_filter_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
-          m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov,
-          a.method == 1 ? sc.sagg : nullptr, npad, a.method == 1 ? sc.egl : nullptr, L.err);
-      L.count(a.method == 1 ? "filter_finish_smoother_reduce" : "filter_finish");
+      if (a.method == 1) {
+        cudaFuncSetAttribute(k_filter_finish<S, NX, NY, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        k_filter_finish<S, NX, NY, true><<<gs, kStageNT, stage_bytes, L.stream>>>(
+            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, sc.sagg, npad, sc.egl,
+            sc.ecap, L.err);
+        L.count("filter_finish_smoother_reduce");
+      } else {
+        cudaFuncSetAttribute(k_filter_finish<S, NX, NY, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        k_filter_finish<S, NX, NY, false><<<gs, kStageNT, stage_bytes, L.stream>>>(
+            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad, nullptr,
+            sc.ecap, L.err);
+        L.count("filter_finish");
+      }
       sc.sagg_valid = a.method == 1;
       break;
     case 2:
@@ -158,9 +192,17 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       }
       break;
     case 3:
+    {
       if (sc.egl == nullptr) return 7;
-      k_smoother_finish<S, NX><<<blocks_for(nch, 128), 128, 0, L.stream>>>(
-          m.t, Lc, nch, sc.sagg, npad, carry, sc.egl, mean, cov);
+      SmoothMaps sm_maps;
+      const int st = make_smooth_maps<S, NX>(sc.egl, sc.ecap, Lc, nfull, mean, cov, sm_maps);
+      if (st) return st;
+      const int smem = kSmoothNT / 32 * SmoothTma<S, NX>::warp + 1024;
+      cudaFuncSetAttribute(k_smoother_finish<S, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem);
+      k_smoother_finish<S, NX><<<blocks_for(nch, kSmoothNT), kSmoothNT, smem, L.stream>>>(
+          m.t, Lc, nch, nfull, sc.sagg, npad, carry, sm_maps, sc.ecap, mean, cov);
+    }
       L.count("smoother_finish");
       sc.sagg_valid = false;
       break;
@@ -186,7 +228,7 @@ static int fast_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, 
                       S* cov, void* (*alloc)(size_t, void*), void* actx) {
   if (m.t == 0) return 0;
   FastScratch<S> sc;
-  int st = fast_prepare_t<S, NX>(m, a, sc, alloc, actx);
+  int st = fast_prepare_t<S, NX, NY>(m, a, sc, alloc, actx);
   if (st) return st;
   const int phases[2][4] = {{0, 1, 2, 3}, {0, 1, 4, 5}};
   const int n = a.method == 0 ? 2 : 4;
@@ -244,7 +286,7 @@ int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, i
 #define PSK_CASE(A, B)                                                           \
   if (m.nx == A && m.ny == B) {                                                  \
     if (phase == 0) {                                                            \
-      int st = fast_prepare_t<S, A>(m, a, *sc, alloc, actx);                    \
+      int st = fast_prepare_t<S, A, B>(m, a, *sc, alloc, actx);                    \
       if (st) return st;                                                         \
     }                                                                            \
     return fast_phase_t<S, A, B>(L, m, a, *sc, phase, mean, cov, carry, elem_out); \

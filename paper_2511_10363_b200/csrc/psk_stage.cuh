@@ -62,6 +62,35 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2,
+                                             const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          map),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// wait until at most N committed bulk groups still READ shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // One staged field: BYTES per step, row = BYTES rounded up to 16, box of
 // kStageNT rows at byte OFF (1024-aligned) of a stage.
 template <int OFF, int BYTES>
@@ -129,12 +158,52 @@ struct FilterTma {
   static constexpr int smem = 2 * stage + 1024 + 64;
 };
 
+// this thread's row of a staged field <- a row-major R x C matrix (the
+// inverse of tma_get, for TMA stores)
+template <class F, typename S, int R, int C>
+__device__ __forceinline__ void tma_put(unsigned char* stage, int t, const Mat<S, R, C>& m) {
+  static_assert(R * C * (int)sizeof(S) == F::bytes && F::bytes % 16 == 0, "field size");
+  const S* o = &m.a[0][0];
+  constexpr int per = 16 / sizeof(S);
+#pragma unroll
+  for (int c = 0; c < R * C / per; ++c) {
+    float4 v;
+    S* vs = reinterpret_cast<S*>(&v);
+#pragma unroll
+    for (int j = 0; j < per; ++j) vs[j] = o[c * per + j];
+    *reinterpret_cast<float4*>(stage + F::off + tma_off<F>(t, c)) = v;
+  }
+}
+
 // Tensor maps of the seven model fields for one staged launch (kernel
 // parameter; `use[f]` = 0 for a broadcast field, read straight from global).
 struct StageMaps {
   CUtensorMap m[7];
   int use[7];
   unsigned tx;  // bytes one stage receives (sum of the used boxes)
+};
+
+// Smoother finish of a warp (32 chunks): TMA loads of the per-step smoothing
+// elements (2-D box {32 chunks, ES components} of the chunk-interleaved
+// buffer) and TMA stores of the smoothed (mean, cov) rows (3-D boxes {row,
+// 1, 32} of the output arrays), both double-buffered.
+struct SmoothMaps {
+  CUtensorMap egl;
+  CUtensorMap mean;
+  CUtensorMap cov;
+  int store;  // 0: rows are not whole 16-byte units -> plain stores
+};
+template <typename S, int NX>
+struct SmoothTma {
+  static constexpr int ES = NX * NX + NX + NX * (NX + 1) / 2;  // EglLayout<NX>::size
+  static constexpr int egl_box = 32 * ES * (int)sizeof(S);
+  static constexpr int egl_stage = (egl_box + 1023) / 1024 * 1024;
+  using Mean = TField<0, NX * (int)sizeof(S)>;  // rows of a 32-row box
+  static constexpr int mean_stage = (Mean::row * 32 + 1023) / 1024 * 1024;
+  using Cov = TField<0, NX * NX * (int)sizeof(S)>;
+  static constexpr int cov_stage = (Cov::row * 32 + 1023) / 1024 * 1024;
+  // one warp: 2 egl stages, 2 mean stages, 2 cov stages, 2 mbarriers
+  static constexpr int warp = 2 * (egl_stage + mean_stage + cov_stage) + 1024;
 };
 
 }  // namespace psk

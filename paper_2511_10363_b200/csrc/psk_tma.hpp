@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "psk_common.cuh"
 #include "psk_stage.cuh"
@@ -30,6 +31,17 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 // complete.  Returns 0, or 9 when a non-broadcast field cannot be described
 // (prepare_model packs every field into a TMA-compatible pitch, so this
 // signals a bug rather than a user error).
+// L2 promotion of the staged boxes (PSK_TMA_L2PROMO = 0..3: none, 64, 128,
+// 256 bytes; default 256) -- an experiment knob for the ncu traffic check.
+inline CUtensorMapL2promotion stage_l2_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char* v = std::getenv("PSK_TMA_L2PROMO");
+    const int i = v ? std::atoi(v) : 3;
+    return static_cast<CUtensorMapL2promotion>(i < 0 || i > 3 ? 3 : i);
+  }();
+  return p;
+}
+
 template <typename S, int NX, int NY>
 int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMaps& maps) {
   using In = FilterTma<S, NX, NY>;
@@ -56,11 +68,57 @@ int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMa
         enc(&maps.m[f],
             sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
             3, const_cast<S*>(base[f]), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            stage_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 9;
     maps.use[f] = 1;
     maps.tx += (unsigned)(row * kStageNT);
   }
+  return 0;
+}
+
+// Tensor maps of the smoother finish: the chunk-interleaved per-step
+// elements egl[(j * ES + comp) * ecap + c] as a 2-D tensor [ecap, ES * L]
+// (box {32, ES}) and the outputs mean[T][NX], cov[T][NX][NX] as 3-D tensors
+// [row, L, nfull] (box {row, 1, 32}).  Rows that are not whole 16-byte units
+// (odd NX in FP64, ...) are stored directly by the kernel (store = 0).
+template <typename S, int NX>
+int make_smooth_maps(const S* egl, long long ecap, long long L, long long nfull, S* mean,
+                     S* cov, SmoothMaps& maps) {
+  using Tm = SmoothTma<S, NX>;
+  auto enc = tma_encoder();
+  if (!enc) return 9;
+  const CUtensorMapDataType dt =
+      sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)ecap, (cuuint64_t)(Tm::ES * L)};
+    cuuint64_t strides[1] = {(cuuint64_t)(ecap * sizeof(S))};
+    cuuint32_t box[2] = {32, (cuuint32_t)Tm::ES};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&maps.egl, dt, 2, const_cast<S*>(egl), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 9;
+  }
+  maps.store = 0;
+  const int mrow = NX * (int)sizeof(S), crow = NX * NX * (int)sizeof(S);
+  if (nfull <= 0 || mrow % 16 || crow % 16 || crow > 256 * (int)sizeof(S) ||
+      reinterpret_cast<uintptr_t>(mean) % 16 || reinterpret_cast<uintptr_t>(cov) % 16)
+    return 0;
+  auto out_map = [&](CUtensorMap* map, S* base, int row) {
+    cuuint64_t dims[3] = {(cuuint64_t)(row / sizeof(S)), (cuuint64_t)L, (cuuint64_t)nfull};
+    cuuint64_t strides[2] = {(cuuint64_t)row, (cuuint64_t)row * (cuuint64_t)L};
+    cuuint32_t box[3] = {(cuuint32_t)(row / sizeof(S)), 1, 32};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapSwizzle sw = row == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : row == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
+    return enc(map, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  };
+  if (!out_map(&maps.mean, mean, mrow) || !out_map(&maps.cov, cov, crow)) return 9;
+  maps.store = 1;
   return 0;
 }
 

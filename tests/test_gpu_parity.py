@@ -78,7 +78,7 @@ def test_exact_bitwise_vs_reference_itself(psk, exact, ref):
 # fast mode: tolerance parity with the sequential oracle
 
 
-@pytest.mark.parametrize("chunk", [1, 3, 8, 32])
+@pytest.mark.parametrize("chunk", [0, 1, 3, 8, 32])
 @pytest.mark.parametrize("t", [1, 2, 5, 64, 100, 1000])
 def test_fast_pkf_prts_ptfs_f64(psk, gpu, port, chunk, t):
     be = psk.CudaBackend(gpu, mode="fast", chunk=chunk)
