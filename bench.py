@@ -49,6 +49,23 @@ def _peaks() -> dict:
     return {"hbm_gbs": HBM_FALLBACK, "src": "fallback (B200_PROFILING.md)"}
 
 
+def _traffic(kernel: str, log2t: int, dtype: str, chunk: int) -> tuple:
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/traffic.json, written by tools/ncu_summary.py --json) when
+    it was taken on this workload; (None, None) otherwise."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        w = d["workload"]
+        if w["log2t"] == log2t and w["dtype"] == dtype and w["chunk"] == chunk:
+            k = d["kernels"].get(kernel)
+            if k is not None:
+                return float(k["dram_bytes"]), d["source"]
+    except (OSError, KeyError, ValueError):
+        pass
+    return None, None
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled (NVML, ~1 kHz) during the timed
     region; falls back to nvidia-smi polling when NVML is unavailable."""
@@ -294,7 +311,9 @@ def run_psk(args) -> None:
         gbs = bps[dom] * steps_local / (avg_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(gbs, 1),
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
-                "traffic": None, "peak_source": peaks["src"],
+                "traffic": _traffic(dom, args.log2t, args.dtype, args.chunk)[0],
+                "traffic_source": _traffic(dom, args.log2t, args.dtype, args.chunk)[1],
+                "peak_source": peaks["src"],
                 "bytes_per_step": bps[dom], "avg_ms": round(avg_ms, 4)}
     kernels = {k: {"avg_ms": round(v[0], 4), "launches_per_step": v[1] // args.steps,
                    "share": round(totals[k] / sum(totals.values()), 4)}

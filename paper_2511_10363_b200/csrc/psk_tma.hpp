@@ -31,15 +31,26 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 // complete.  Returns 0, or 9 when a non-broadcast field cannot be described
 // (prepare_model packs every field into a TMA-compatible pitch, so this
 // signals a bug rather than a user error).
-// L2 promotion of the staged boxes (PSK_TMA_L2PROMO = 0..3: none, 64, 128,
-// 256 bytes; default 256) -- an experiment knob for the ncu traffic check.
-inline CUtensorMapL2promotion stage_l2_promotion() {
-  static const CUtensorMapL2promotion p = [] {
+// L2 promotion of the staged boxes (experiment knobs for the ncu traffic
+// check, 0..3 = none / 64 / 128 / 256 bytes): PSK_TMA_L2PROMO for rows of 64
+// bytes and more (default 256), PSK_TMA_L2PROMO_SMALL for smaller rows
+// (default none).  A promoted 256-byte line holds 8-16 steps of a 16/32-byte
+// field of ONE chunk; the walk needs them over ~50 us, by which time ~300 MB
+// have streamed through the 126 MB L2, so most of the promotion is evicted
+// unused (profiles/r01_v4: finish reads 8.36 GB for 6.98 GB of inputs with
+// 256 B everywhere; small rows unpromoted: 4.72 vs 4.89 ms per PRTS).
+inline CUtensorMapL2promotion stage_l2_promotion(int row) {
+  static const int big = [] {
     const char* v = std::getenv("PSK_TMA_L2PROMO");
     const int i = v ? std::atoi(v) : 3;
-    return static_cast<CUtensorMapL2promotion>(i < 0 || i > 3 ? 3 : i);
+    return i < 0 || i > 3 ? 3 : i;
   }();
-  return p;
+  static const int small = [] {
+    const char* v = std::getenv("PSK_TMA_L2PROMO_SMALL");
+    const int i = v ? std::atoi(v) : 0;
+    return i < 0 || i > 3 ? 3 : i;
+  }();
+  return static_cast<CUtensorMapL2promotion>(row >= 64 ? big : small);
 }
 
 template <typename S, int NX, int NY>
@@ -68,7 +79,7 @@ int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMa
         enc(&maps.m[f],
             sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
             3, const_cast<S*>(base[f]), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-            stage_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            stage_l2_promotion(row), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 9;
     maps.use[f] = 1;
     maps.tx += (unsigned)(row * kStageNT);

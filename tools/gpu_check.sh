@@ -30,7 +30,7 @@ if has ncu; then
     --log-file $O/launches.csv python bench.py $NCU_ARGS > $O/ncu_launches.log 2>&1
   echo "rc=$?" >> $O/ncu_launches.log
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k "regex:${NCU_KERNEL:-k_filter_finish}" -s ${NCU_SKIP:-1} -c 1 -f -o $O/prof \
+    -k "regex:${NCU_KERNEL:-k_filter_reduce|k_filter_finish|k_smoother_finish}" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-3} -f -o $O/prof \
     python bench.py $NCU_ARGS > $O/ncu_full.log 2>&1
   echo "rc=$?" >> $O/ncu_full.log
   tail -3 $O/ncu_full.log

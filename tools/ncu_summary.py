@@ -91,7 +91,37 @@ def _scale(unit: str) -> float:
             "GB": 1e9}.get(unit, 1.0)
 
 
+KNAMES = {"k_filter_reduce": "filter_reduce", "k_filter_finish": "filter_finish_smoother_reduce",
+          "k_smoother_finish": "smoother_finish", "k_dlb": "chunk_scan_dlb"}
+
+
+def traffic_json(path: str, source: str, workload: dict) -> dict:
+    """{bench kernel name: {"dram_bytes": read + write per launch}} of a capture"""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    u = dict(zip(hdr, units))
+    out = {}
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        name = d.get("Kernel Name", "").split("<")[0].split("(")[0].strip().split(" ")[-1]
+        key = KNAMES.get(name)
+        if key is None:
+            continue
+        b = float(d["dram__bytes_read.sum"]) * _scale(u["dram__bytes_read.sum"]) + \
+            float(d["dram__bytes_write.sum"]) * _scale(u["dram__bytes_write.sum"])
+        out[key] = {"dram_bytes": b}
+    return {"source": source, "workload": workload, "kernels": out}
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--json":  # --json <prof.ncu-rep> <source> <log2t> <dtype> <chunk>
+        import json
+        print(json.dumps(traffic_json(sys.argv[2], sys.argv[3],
+                                      {"log2t": int(sys.argv[4]), "dtype": sys.argv[5],
+                                       "chunk": int(sys.argv[6])}), indent=1))
+        sys.exit(0)
     print(launches(sys.argv[1]))
     if len(sys.argv) > 2:
         print()
