@@ -4,6 +4,7 @@
 // path: every numeric result comes from the CUDA kernels.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -102,6 +103,29 @@ struct Field {
   const char* name;
 };
 
+// dst[k * dp + b] = src[k * sp + b] for b < bytes, k < rows (4-byte units:
+// every block and pitch here is a multiple of sizeof(float))
+__global__ void k_repitch(unsigned* dst, long long dp, const unsigned* src, long long sp,
+                          int words, long long rows) {
+  const long long n = rows * words;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long k = i / words;
+    const int w = (int)(i - k * words);
+    dst[k * dp + w] = src[k * sp + w];
+  }
+}
+cudaError_t repitch(void* dst, size_t dpitch, const void* src, size_t spitch, size_t bytes,
+                    long long rows, cudaStream_t stream) {
+  const int words = (int)(bytes / 4);
+  const long long n = rows * words;
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 32);
+  k_repitch<<<grid < 1 ? 1 : grid, 256, 0, stream>>>(
+      static_cast<unsigned*>(dst), (long long)(dpitch / 4), static_cast<const unsigned*>(src),
+      (long long)(spitch / 4), words, rows);
+  return cudaGetLastError();
+}
+
 // Resolve a model into a device ModelView<S>: device inputs are used in place
 // when 16-byte aligned, host (or misaligned) inputs are packed into dense
 // device arrays (time-invariant fields keep a single block, stride 0).
@@ -142,12 +166,23 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     S* dst = static_cast<S*>(ctx_alloc(pb * (size_t)nblk, ctx));
     if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
     const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    cudaError_t e;
-    if (st != 0 && pb == bb && st == f[i].block) {
+    cudaError_t e = cudaSuccess;
+    const size_t sp = st == 0 ? bb : sizeof(S) * (size_t)st;  // source pitch (bytes)
+    if (st != 0 && pb == bb && sp == bb) {
       e = cudaMemcpyAsync(dst, f[i].src, bb * (size_t)nblk, kind, ctx->stream);
+    } else if (st == 0 || nblk == 1) {
+      e = cudaMemcpyAsync(dst, f[i].src, bb, kind, ctx->stream);
     } else {
-      e = cudaMemcpy2DAsync(dst, pb, f[i].src, st == 0 ? bb : sizeof(S) * (size_t)st, bb,
-                            (size_t)nblk, kind, ctx->stream);
+      // re-pitch on the device (a 2-D memcpy with rows of a few bytes runs
+      // far below HBM speed: 3.7 ms for the two 8-byte FP32 fields at 2^24)
+      const void* src = f[i].src;
+      if (host) {  // dense H2D of the source span first
+        void* tmp = ctx_alloc(sp * (size_t)nblk, ctx);
+        if (!tmp) return fail(PSK_E_ALLOC, "device allocation failed (model staging)");
+        e = cudaMemcpyAsync(tmp, src, sp * (size_t)(nblk - 1) + bb, kind, ctx->stream);
+        src = tmp;
+      }
+      if (e == cudaSuccess) e = repitch(dst, pb, src, sp, bb, nblk, ctx->stream);
     }
     if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("model copy: ") + cuda_msg(e));
     outp[i] = dst;

@@ -586,7 +586,7 @@ __device__ __forceinline__ SElem<S, NX> terminal_elem(const Vec<S, NX>& x,
 
 // reduce: chunk c = steps [c L, min(c L + L, T)) -> one filtering element
 template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(kStageNT, 2)
+__global__ void __launch_bounds__(kStageNT, sizeof(S) == 8 ? 2 : 3)
     k_filter_reduce(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
                     long long nchunks, long long nfull, S* agg, long long cap, unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
