@@ -251,6 +251,7 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     if (!dmean || !dcov) return fail(PSK_E_ALLOC, "device allocation failed (outputs)");
   }
   ExactLaunch& L = ctx->launch;
+  bool done = false;  // served by a fast (register-resident or wide) path
   if (ctx->mode == PSK_MODE_FAST && fast_supported<S>(m->nx, m->ny)) {
     FastArgs a;
     a.method = method;
@@ -262,11 +263,30 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
     if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
     if (st) return fail(PSK_E_CUDA, "fast path failed");
-  } else {
-    if (alg == PSK_DECOUPLED_LOOKBACK)
-      return fail(PSK_E_CONTRACT,
-                  "decoupled look-back is a fast-path scan (not in the "
-                  "reference's level-by-level set)");
+    done = true;
+  }
+  if (!done && ctx->mode == PSK_MODE_FAST) {
+    // dims without a register-resident instantiation: warp-per-chunk kernels
+    FastArgs a;
+    a.method = method;
+    a.alg = alg;
+    a.sengupta_n = sengupta_n;
+    a.chunk = ctx->chunk;
+    a.waves = ctx->waves;
+    st = wide_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
+    if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
+    if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (wide scan)");
+    if (st > 0) return fail(PSK_E_CUDA, "wide fast path failed");
+    done = st == 0;
+  }
+  if (!done) {
+    if (alg == PSK_DECOUPLED_LOOKBACK) {
+      if (ctx->mode != PSK_MODE_FAST)
+        return fail(PSK_E_CONTRACT,
+                    "decoupled look-back is a fast-path scan (not in the "
+                    "reference's level-by-level set)");
+      alg = PSK_INPLACE_LAFI;  // fast mode, uncovered request (wide PTFS)
+    }
     const unsigned long long n = alg == PSK_SEQUENTIAL ? T : next_pow2(T);
     ScanPlan plan = make_scan_plan(alg, sengupta_n, (long long)n);
     if (plan.status) return fail(PSK_E_CONTRACT, plan.why);

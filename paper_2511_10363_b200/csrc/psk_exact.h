@@ -62,6 +62,12 @@ template <typename S>
 int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a,
              S* mean, S* cov, void* (*alloc)(size_t, void*), void* alloc_ctx);
 
+// wide fast path (psk_wide_impl.cuh): runtime nx, ny <= 16, PKF and PRTS;
+// returns -1 when the request is not covered (PTFS -> exact path)
+template <typename S>
+int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
+             void* (*alloc)(size_t, void*), void* alloc_ctx);
+
 template <typename S>
 int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
                      void** scratch, S* mean, S* cov, const S* carry, S* elem_out,

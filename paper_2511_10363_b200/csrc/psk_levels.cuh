@@ -40,11 +40,14 @@ __device__ __forceinline__ void h_assign(const Ops& ops,
   ops.assign(dst, dst.phys(di), src, src.phys(si));
 }
 
-template <class Ops>
+// UNIT = threads per iteration: 1 (one thread per combine, register-resident
+// operators) or 32 (one warp per combine: the warp-cooperative operators of
+// psk_wide.cuh; every lane of the warp runs the same iteration).
+template <class Ops, int UNIT = 1>
 __global__ void __launch_bounds__(128) k_level(Ops ops, Bufs3<Ops> bufs,
                                                LevelDesc d) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x / UNIT;
+  for (long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / UNIT;
        m < d.count; m += stride) {
     switch (d.kind) {
       case kLvSeqChain: {

@@ -100,12 +100,43 @@ def test_fast_pkf_prts_ptfs_f64(psk, gpu, port, chunk, t):
 def test_fast_other_dims(psk, fast, port, nx, ny):
     m, ys = gen(port, 100 + nx * 10 + ny, nx, ny, 200)
     rts = port.rts_run(m, ys)
-    # dims without a fast instantiation run the level-by-level kernels, which
-    # have no decoupled look-back (a fast-path-only scan)
-    algs = (3, 6) if nx <= 4 else (3,)
-    for alg in algs:
+    # dims without a register-resident instantiation run the wide
+    # (warp-per-chunk) kernels; DLB requests map to the LaFi plan there
+    for alg in (3, 6):
         got = psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg(alg), 4), fast)
         assert max_rel_err(got.mean, got.cov, *rts) < TOL64, (nx, ny, alg)
+
+
+@pytest.mark.parametrize("nx,ny", [(5, 2), (6, 3), (8, 8), (12, 5), (16, 8), (16, 16), (7, 1)])
+@pytest.mark.parametrize("chunk", [0, 1, 5])
+def test_wide_path_all_methods(psk, gpu, port, nx, ny, chunk):
+    """nx up to kMaxDim = 16 (mat.hpp:19): the warp-per-chunk kernels for
+    PKF/PRTS (PTFS falls back to the level-by-level kernels), every ScanAlg,
+    vs the sequential oracle at the FP64 gate."""
+    be = psk.CudaBackend(gpu, mode="fast", chunk=chunk)
+    m, ys = gen(port, 300 + nx * 17 + ny, nx, ny, 150)
+    kf = port.kf_run(m, ys)
+    rts = port.rts_run(m, ys)
+    for alg in FAST_ALGS:
+        spec = psk.ScanSpec(psk.ScanAlg(alg), 4)
+        got = psk.pkf_run(m, ys, spec, be)
+        assert max_rel_err(got.mean, got.cov, *kf) < TOL64, ("pkf", alg)
+        got = psk.prts_run(m, ys, spec, be)
+        assert max_rel_err(got.mean, got.cov, *rts) < TOL64, ("prts", alg)
+    got = psk.ptfs_run(m, ys, psk.ScanSpec(psk.ScanAlg(6), 4), be)
+    assert max_rel_err(got.mean, got.cov, *rts) < TOL64, "ptfs"
+    be.set_profile(True)
+    psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg(6)), be)
+    assert any(n.startswith("wide_") for n, _ in be.last_profile())
+
+
+def test_wide_path_large_t(psk, gpu, port):
+    """nx = 16, ny = 8 (BASELINE configs[4] shape) over many chunks."""
+    be = psk.CudaBackend(gpu, mode="fast")
+    m, ys = gen(port, 77, 16, 8, 20000)
+    rts = port.rts_run(m, ys)
+    got = psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg.DecoupledLookback), be)
+    assert max_rel_err(got.mean, got.cov, *rts) < TOL64
 
 
 def test_fast_many_seeds_acceptance(psk, fast, port):
