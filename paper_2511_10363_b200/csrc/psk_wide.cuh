@@ -5,9 +5,9 @@
 // At nx = 16 a filtering element is 3 nx^2 + 2 nx = 800 scalars (6.4 KB in
 // FP64) -- it cannot live in one thread's registers (hard part
 // 1), so every matrix of a chunk lives in the warp's shared-memory slots and
-// the 32 lanes cooperate on each operation: products (lanes over output
-// entries), Cholesky / pivoted LU (sequential over columns, lanes over rows),
-// triangular solves (lanes over right-hand-side columns).  Per step the work
+// the 32 lanes cooperate on each operation: products (each lane a 2 x 4
+// register tile of the output) and solves / inverses (Gauss-Jordan on an
+// augmented block, each pivot step lane-parallel over the trailing block).  Per step the work
 // is ~40 k flops (make_filter_element 40 676, Lemma-1 combine
 // 88 624 at nx = 16), so the warp is busy; per-step model blocks are
 // contiguous in the reference layout and a warp reads each with one
@@ -43,185 +43,187 @@ __device__ __forceinline__ WM<S> vec(S* p) { return WM<S>{p, 1}; }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-// C[n x m] = (Z or 0) + sgn * op(A) op(B), op(X) = X or X^T; inner dim k.
-// C must not alias A or B (it may alias Z: each entry reads Z first).
-template <typename S>
-__device__ __forceinline__ void gemm(WM<S> C, WM<S> A, bool tA, WM<S> B, bool tB, int n, int k,
-                                     int m, const S* z = nullptr, int zld = 0, S sgn = S(1),
+// Element loops without integer division (runtime divisors cost ~20
+// instructions each and dominated the first version's instruction mix,
+// profiles/r01_v6): for m <= 16 lane l covers column l & 15 of rows
+// l >> 4, l >> 4 + 2, ...; wider blocks go row by row, lanes over columns.
+template <class Fn>
+__device__ __forceinline__ void for_each(int n, int m, Fn&& fn) {
+  const int ln = lane_id();
+  if (m <= 16) {
+    const int c = ln & 15;
+    if (c < m)
+      for (int r = ln >> 4; r < n; r += 2) fn(r, c);
+  } else {
+    for (int r = 0; r < n; ++r)
+      for (int c = ln; c < m; c += 32) fn(r, c);
+  }
+}
+
+// C[n x m] = (Z or 0) + sgn * op(A) op(B), op(X) = X or X^T (TA, TB); inner
+// dim k.  Register-blocked: each lane owns a 2 x 4 tile of C (8 independent
+// accumulators: a one-output-per-lane dot product is a chain of dependent
+// FMAs), operands walked by pointer increments; a matrix-vector product uses
+// lanes over rows with 4 partial sums.  `sym`: the result is symmetric --
+// tiles below the diagonal are skipped and the upper triangle is mirrored.
+// C must not alias A or B (it may alias Z entry-wise).
+template <bool TA, bool TB, typename S>
+__device__ __forceinline__ void gemm(WM<S> C, WM<S> A, WM<S> B, int n, int k, int m,
+                                     const S* z = nullptr, int zld = 0, S sgn = S(1),
                                      bool sym = false) {
-  for (int idx = lane_id(); idx < n * m; idx += 32) {
-    const int r = idx / m, c = idx - (idx / m) * m;
-    if (sym && c < r) continue;  // symmetric result: upper triangle, mirrored below
-    S acc = z ? z[r * zld + c] : S(0);
-    for (int q = 0; q < k; ++q) {
-      const S a = tA ? A(q, r) : A(r, q);
-      const S b = tB ? B(c, q) : B(q, c);
-      acc = sfma(sgn * a, b, acc);
+  const int as = TA ? A.ld : 1;   // step of op(A)(r, q) in q
+  const int bs = TB ? 1 : B.ld;   // step of op(B)(q, c) in q
+  if (m == 1) {
+    for (int r = lane_id(); r < n; r += 32) {
+      const S* pa = TA ? &A(0, r) : &A(r, 0);
+      const S* pb = &B(0, 0);
+      S acc[4] = {S(0), S(0), S(0), S(0)};
+      int q = 0;
+      for (; q + 4 <= k; q += 4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = sfma(pa[(q + j) * as], pb[(q + j) * bs], acc[j]);
+      }
+      for (; q < k; ++q) acc[0] = sfma(pa[q * as], pb[q * bs], acc[0]);
+      const S sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      C(r, 0) = sfma(sgn, sum, z ? z[r * zld] : S(0));
     }
-    C(r, c) = acc;
-    if (sym) C(c, r) = acc;
+    __syncwarp();
+    return;
+  }
+  const int tr = (n + 1) >> 1, tc = (m + 3) >> 2;
+  for (int t = lane_id(); t < tr * tc; t += 32) {
+    const int r0 = (t / tc) * 2, c0 = (t - (t / tc) * tc) * 4;
+    if (sym && c0 + 3 < r0) continue;  // entirely below the diagonal
+    const int r1 = min(r0 + 1, n - 1);
+    const S* pa0 = TA ? &A(0, r0) : &A(r0, 0);
+    const S* pa1 = TA ? &A(0, r1) : &A(r1, 0);
+    const S* pb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cj = min(c0 + j, m - 1);
+      pb[j] = TB ? &B(cj, 0) : &B(0, cj);
+    }
+    S acc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = S(0);
+#pragma unroll 4
+    for (int q = 0; q < k; ++q) {
+      const S a0 = pa0[q * as], a1 = pa1[q * as];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const S b = pb[j][q * bs];
+        acc[0][j] = sfma(a0, b, acc[0][j]);
+        acc[1][j] = sfma(a1, b, acc[1][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + i, c = c0 + j;
+        if (r < n && c < m && (!sym || c >= r))
+          C(r, c) = sfma(sgn, acc[i][j], z ? z[r * zld + c] : S(0));
+      }
   }
   __syncwarp();
+  if (sym) {
+    for_each(n, n, [&](int r, int c) {
+      if (c < r) C(r, c) = C(c, r);
+    });
+    __syncwarp();
+  }
 }
 template <typename S>
 __device__ __forceinline__ void copy(WM<S> D, WM<S> A, int n, int m) {
-  for (int idx = lane_id(); idx < n * m; idx += 32) {
-    const int r = idx / m, c = idx - (idx / m) * m;
-    D(r, c) = A(r, c);
-  }
+  for_each(n, m, [&](int r, int c) { D(r, c) = A(r, c); });
   __syncwarp();
 }
 template <typename S>
 __device__ __forceinline__ void fill(WM<S> D, int n, int m, S diag, S off) {
-  for (int idx = lane_id(); idx < n * m; idx += 32) {
-    const int r = idx / m, c = idx - (idx / m) * m;
-    D(r, c) = r == c ? diag : off;
-  }
+  for_each(n, m, [&](int r, int c) { D(r, c) = r == c ? diag : off; });
   __syncwarp();
 }
-// coalesced load of a contiguous row-major r x c block from global
+// coalesced load / store of a contiguous row-major n x m block in global
 template <typename S>
 __device__ __forceinline__ void gload(WM<S> D, const S* g, int n, int m) {
-  for (int idx = lane_id(); idx < n * m; idx += 32) {
-    const int r = idx / m, c = idx - (idx / m) * m;
-    D(r, c) = g[idx];
-  }
+  for_each(n, m, [&](int r, int c) { D(r, c) = g[r * m + c]; });
 }
 template <typename S>
 __device__ __forceinline__ void gstore(S* g, WM<S> A, int n, int m) {
-  for (int idx = lane_id(); idx < n * m; idx += 32) {
-    const int r = idx / m, c = idx - (idx / m) * m;
-    g[idx] = A(r, c);
-  }
+  for_each(n, m, [&](int r, int c) { g[r * m + c] = A(r, c); });
 }
 
-// Cholesky A = L L^T (mat.hpp:153-175): L lower (upper part unused), inv[j]
-// = 1 / L(j,j).  Sequential over columns, lanes over the rows below.
+// Gauss-Jordan elimination on the augmented n x w matrix X = [A | B]
+// (n <= 16, w <= 64): the left block is reduced to I and the same row
+// operations turn the right block into A^-1 B.  Column-oriented and
+// register-resident: lane l holds columns l and l + 32 in registers, every
+// pivot step broadcasts the pivot column with shuffles and each lane updates
+// its columns with independent FMAs (the shared-memory formulation spent
+// half of k_wide_finish in load/store chains of this elimination,
+// profiles/r01_v6).  The pivot loop is unrolled so every register index is
+// static.  pivot = false: A symmetric positive definite, no row exchanges
+// (elimination on an SPD matrix is stable; a non-positive pivot raises
+// kErrNotPD as the reference's Cholesky does, mat.hpp:165); pivot = true:
+// partial pivoting on the first maximum |a(r, p)| (mat.hpp:180-205), a zero
+// pivot raises kErrSingular.
 template <typename S>
-__device__ __forceinline__ void chol(WM<S> L, S* inv, WM<S> A, int n, unsigned& err) {
-  for (int j = 0; j < n; ++j) {
-    S d = A(j, j);
-    for (int q = 0; q < j; ++q) d = sfma(-L(j, q), L(j, q), d);
-    if (!(d > S(0))) err |= kErrNotPD;
-    const S il = srsqrt(d);
-    for (int i = j + lane_id(); i < n; i += 32) {
-      if (i == j) {
-        L(j, j) = d * il;
-        inv[j] = il;
-      } else {
-        S acc = A(i, j);
-        for (int q = 0; q < j; ++q) acc = sfma(-L(i, q), L(j, q), acc);
-        L(i, j) = acc * il;
-      }
-    }
-    __syncwarp();
-  }
-}
-// X[n x m] = (L L^T)^-1 B; lanes over columns (X may alias B)
-template <typename S>
-__device__ __forceinline__ void chol_solve(WM<S> X, WM<S> L, const S* inv, WM<S> B, int n,
-                                           int m) {
-  for (int c = lane_id(); c < m; c += 32) {
-    for (int i = 0; i < n; ++i) {
-      S acc = B(i, c);
-      for (int q = 0; q < i; ++q) acc = sfma(-L(i, q), X(q, c), acc);
-      X(i, c) = acc * inv[i];
-    }
-    for (int i = n - 1; i >= 0; --i) {
-      S acc = X(i, c);
-      for (int q = i + 1; q < n; ++q) acc = sfma(-L(q, i), X(q, c), acc);
-      X(i, c) = acc * inv[i];
-    }
-  }
-  __syncwarp();
-}
-
-// LU with partial pivoting (mat.hpp:177-205): LU holds unit-lower L and U,
-// inv[c] = 1 / U(c,c), piv[c] = row swapped into c at step c (first maximum
-// of |a(r,c)|, as the reference).
-template <typename S>
-__device__ __forceinline__ void lu(WM<S> LU, S* inv, int* piv, int n, unsigned& err) {
+__device__ __forceinline__ void gauss_jordan(WM<S> X, int n, int w, bool pivot, unsigned& err) {
   const int ln = lane_id();
-  for (int c = 0; c < n; ++c) {
-    // argmax over rows c..n-1 (lowest index on ties)
-    S best = S(-1);
-    int p = c;
-    for (int r = c + ln; r < n; r += 32) {
-      const S v = sabs(LU(r, c));
-      if (v > best) { best = v; p = r; }
-    }
+  const bool has0 = ln < w, has1 = ln + 32 < w;
+  S x0[kMaxN], x1[kMaxN];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const S ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int op = __shfl_xor_sync(0xffffffffu, p, o);
-      if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
-    }
-    if (ln == 0) piv[c] = p;
-    if (best == S(0)) err |= kErrSingular;
-    if (p != c)
-      for (int j = ln; j < n; j += 32) {
-        const S t = LU(c, j);
-        LU(c, j) = LU(p, j);
-        LU(p, j) = t;
-      }
-    __syncwarp();
-    const S ip = srcp(LU(c, c));
-    if (ln == 0) inv[c] = ip;
-    for (int r = c + 1 + ln; r < n; r += 32) LU(r, c) *= ip;
-    __syncwarp();
-    const int w = n - c - 1;
-    for (int idx = ln; idx < w * w; idx += 32) {
-      const int r = c + 1 + idx / w, j = c + 1 + idx % w;
-      LU(r, j) = sfma(-LU(r, c), LU(c, j), LU(r, j));
-    }
-    __syncwarp();
+  for (int i = 0; i < kMaxN; ++i) {
+    x0[i] = (i < n && has0) ? X(i, ln) : S(0);
+    x1[i] = (i < n && has1) ? X(i, ln + 32) : S(0);
   }
-}
-// X = M^-1 B (trans = false) or M^-T B (trans = true); lanes over columns
-template <typename S>
-__device__ __forceinline__ void lu_solve(WM<S> X, WM<S> LU, const S* inv, const int* piv,
-                                         WM<S> B, int n, int m, bool trans) {
-  for (int c = lane_id(); c < m; c += 32) {
-    if (!trans) {
-      for (int i = 0; i < n; ++i) X(i, c) = B(i, c);
-      for (int q = 0; q < n; ++q) {
-        const int p = piv[q];
-        if (p != q) {
-          const S t = X(q, c);
-          X(q, c) = X(p, c);
-          X(p, c) = t;
-        }
-      }
-      for (int i = 1; i < n; ++i) {
-        S acc = X(i, c);
-        for (int q = 0; q < i; ++q) acc = sfma(-LU(i, q), X(q, c), acc);
-        X(i, c) = acc;
-      }
-      for (int i = n - 1; i >= 0; --i) {
-        S acc = X(i, c);
-        for (int q = i + 1; q < n; ++q) acc = sfma(-LU(i, q), X(q, c), acc);
-        X(i, c) = acc * inv[i];
-      }
-    } else {
-      for (int i = 0; i < n; ++i) {  // U^T z = b
-        S acc = B(i, c);
-        for (int q = 0; q < i; ++q) acc = sfma(-LU(q, i), X(q, c), acc);
-        X(i, c) = acc * inv[i];
-      }
-      for (int i = n - 1; i >= 0; --i) {  // L^T w = z
-        S acc = X(i, c);
-        for (int q = i + 1; q < n; ++q) acc = sfma(-LU(q, i), X(q, c), acc);
-        X(i, c) = acc;
-      }
-      for (int q = n - 1; q >= 0; --q) {  // undo the interchanges
-        const int p = piv[q];
-        if (p != q) {
-          const S t = X(q, c);
-          X(q, c) = X(p, c);
-          X(p, c) = t;
-        }
+#pragma unroll
+  for (int p = 0; p < kMaxN; ++p) {
+    if (p >= n) break;
+    if (pivot) {
+      // lane p holds the pivot column: first maximum of |x(i, p)|, i >= p
+      S best = S(-1);
+      int pr = p;
+#pragma unroll
+      for (int i = p; i < kMaxN; ++i)
+        if (i < n && sabs(x0[i]) > best) { best = sabs(x0[i]); pr = i; }
+      pr = __shfl_sync(0xffffffffu, pr, p);
+      best = __shfl_sync(0xffffffffu, best, p);
+      if (best == S(0)) err |= kErrSingular;
+      if (pr != p) {  // warp-uniform: swap rows p and pr in every column
+        S a0 = x0[p], a1 = x1[p];
+#pragma unroll
+        for (int i = p + 1; i < kMaxN; ++i)
+          if (i == pr) {
+            x0[p] = x0[i];
+            x1[p] = x1[i];
+            x0[i] = a0;
+            x1[i] = a1;
+          }
       }
     }
+    const S d = __shfl_sync(0xffffffffu, x0[p], p);
+    if (!pivot && !(d > S(0))) err |= kErrNotPD;
+    const S ip = srcp(d);
+    const S r0 = x0[p] * ip, r1 = x1[p] * ip;  // scaled pivot row (my columns)
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i) {
+      if (i >= n) break;
+      const S f = __shfl_sync(0xffffffffu, x0[i], p);  // pivot column entry
+      if (i != p) {
+        x0[i] = sfma(-f, r0, x0[i]);
+        x1[i] = sfma(-f, r1, x1[i]);
+      }
+    }
+    x0[p] = r0;
+    x1[p] = r1;
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxN; ++i) {
+    if (i >= n) break;
+    if (has0) X(i, ln) = x0[i];
+    if (has1) X(i, ln + 32) = x1[i];
   }
   __syncwarp();
 }

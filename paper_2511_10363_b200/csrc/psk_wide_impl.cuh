@@ -81,33 +81,39 @@ __device__ void filter_combine(S* o, const S* l, const S* r, int n, Slots<S> sc,
   const FOffs F(n);
   auto M = [&](const S* p, int off) { return WM<S>{const_cast<S*>(p) + off, n}; };
   auto V = [&](const S* p, int off) { return WM<S>{const_cast<S*>(p) + off, 1}; };
-  WM<S> lu_m = mat(sc.m(m0)), t1 = mat(sc.m(m0 + 1)), t2 = mat(sc.m(m0 + 2));
-  S* inv = sc.v(v0);
+  // [M | I] with M = I + C_l J_r (2 slots) -> [I | M^-1] by Gauss-Jordan with
+  // partial pivoting; N = I + J_r C_l = M^T (C, J symmetric), so
+  // N^-1 = (M^-1)^T and every solve of Lemma 1 becomes a product
+  WM<S> aug{sc.m(m0), 2 * n};
+  WM<S> t1 = mat(sc.m(m0 + 2)), t2 = mat(sc.m(m0 + 3));
   WM<S> u1 = vec(sc.v(v0 + 1)), u2 = vec(sc.v(v0 + 2));
-  int* piv = sc.piv();
-  // M = I + C_l J_r, factored once; N = I + J_r C_l = M^T (C, J symmetric)
-  gemm(lu_m, M(l, F.C), false, M(r, F.J), false, n, n, n);
-  add_eye(lu_m, n);
-  lu(lu_m, inv, piv, n, err);
+  gemm<false, false>(aug, M(l, F.C), M(r, F.J), n, n, n);
+  for_each(n, n, [&](int i, int j) {
+    aug(i, n + j) = i == j ? S(1) : S(0);
+    if (i == j) aug(i, i) += S(1);
+  });
+  __syncwarp();
+  gauss_jordan(aug, n, 2 * n, true, err);
+  const WM<S> Mi{aug.p + n, 2 * n};
   // A' = A_r M^-1 A_l
-  lu_solve(t1, lu_m, inv, piv, M(l, F.A), n, n, false);
-  gemm(M(o, F.A), M(r, F.A), false, t1, false, n, n, n);
+  gemm<false, false>(t1, Mi, M(l, F.A), n, n, n);
+  gemm<false, false>(M(o, F.A), M(r, F.A), t1, n, n, n);
   // b' = A_r M^-1 (C_l eta_r + b_l) + b_r
-  gemm(u1, M(l, F.C), false, V(r, F.eta), false, n, n, 1, l + F.b, 1);
-  lu_solve(u2, lu_m, inv, piv, u1, n, 1, false);
-  gemm(V(o, F.b), M(r, F.A), false, u2, false, n, n, 1, r + F.b, 1);
+  gemm<false, false>(u1, M(l, F.C), V(r, F.eta), n, n, 1, l + F.b, 1);
+  gemm<false, false>(u2, Mi, u1, n, n, 1);
+  gemm<false, false>(V(o, F.b), M(r, F.A), u2, n, n, 1, r + F.b, 1);
   // C' = A_r M^-1 C_l A_r^T + C_r (symmetric)
-  lu_solve(t1, lu_m, inv, piv, M(l, F.C), n, n, false);
-  gemm(t2, M(r, F.A), false, t1, false, n, n, n);
-  gemm(M(o, F.C), t2, false, M(r, F.A), true, n, n, n, r + F.C, n, S(1), true);
+  gemm<false, false>(t1, Mi, M(l, F.C), n, n, n);
+  gemm<false, false>(t2, M(r, F.A), t1, n, n, n);
+  gemm<false, true>(M(o, F.C), t2, M(r, F.A), n, n, n, r + F.C, n, S(1), true);
   // eta' = A_l^T M^-T (eta_r - J_r b_l) + eta_l
-  gemm(u1, M(r, F.J), false, V(l, F.b), false, n, n, 1, r + F.eta, 1, S(-1));
-  lu_solve(u2, lu_m, inv, piv, u1, n, 1, true);
-  gemm(V(o, F.eta), M(l, F.A), true, u2, false, n, n, 1, l + F.eta, 1);
+  gemm<false, false>(u1, M(r, F.J), V(l, F.b), n, n, 1, r + F.eta, 1, S(-1));
+  gemm<true, false>(u2, Mi, u1, n, n, 1);
+  gemm<true, false>(V(o, F.eta), M(l, F.A), u2, n, n, 1, l + F.eta, 1);
   // J' = A_l^T M^-T J_r A_l + J_l (symmetric)
-  lu_solve(t1, lu_m, inv, piv, M(r, F.J), n, n, true);
-  gemm(t2, t1, false, M(l, F.A), false, n, n, n);
-  gemm(M(o, F.J), M(l, F.A), true, t2, false, n, n, n, l + F.J, n, S(1), true);
+  gemm<true, false>(t1, Mi, M(r, F.J), n, n, n);
+  gemm<false, false>(t2, t1, M(l, F.A), n, n, n);
+  gemm<true, false>(M(o, F.J), M(l, F.A), t2, n, n, n, l + F.J, n, S(1), true);
 }
 // Lemma 2 (kalman_elems.hpp:396-418): E' = E_l E_r, g' = E_l g_r + g_l,
 // L' = E_l L_r E_l^T + L_l; scratch: 1 matrix slot
@@ -117,10 +123,10 @@ __device__ void smoother_combine(S* o, const S* l, const S* r, int n, Slots<S> s
   auto M = [&](const S* p, int off) { return WM<S>{const_cast<S*>(p) + off, n}; };
   auto V = [&](const S* p, int off) { return WM<S>{const_cast<S*>(p) + off, 1}; };
   WM<S> t = mat(sc.m(m0));
-  gemm(M(o, F.E), M(l, F.E), false, M(r, F.E), false, n, n, n);
-  gemm(V(o, F.g), M(l, F.E), false, V(r, F.g), false, n, n, 1, l + F.g, 1);
-  gemm(t, M(l, F.E), false, M(r, F.L), false, n, n, n);
-  gemm(M(o, F.L), t, false, M(l, F.E), true, n, n, n, l + F.L, n, S(1), true);
+  gemm<false, false>(M(o, F.E), M(l, F.E), M(r, F.E), n, n, n);
+  gemm<false, false>(V(o, F.g), M(l, F.E), V(r, F.g), n, n, 1, l + F.g, 1);
+  gemm<false, false>(t, M(l, F.E), M(r, F.L), n, n, n);
+  gemm<false, true>(M(o, F.L), t, M(l, F.E), n, n, n, l + F.L, n, S(1), true);
 }
 
 // ---- scan operator policies (warp-cooperative, AoS global buffers) --------
@@ -244,23 +250,26 @@ struct Step {
 template <typename S>
 __device__ void cond_update(const Step<S>& st, unsigned& err) {
   const int nx = st.nx, ny = st.ny;
-  WM<S> hc = st.T(0), s = st.T(1), lch = st.T(2), kt = st.T(3), ha = st.T(4), w = st.T(5);
-  WM<S> v = st.t(0), sv = st.t(1);
-  S* inv = st.sc.v(5 + 2);
-  gemm(hc, st.H(), false, st.C(), false, ny, nx, nx);
-  gemm(s, hc, false, st.H(), true, ny, nx, ny, st.R().p, kLd, S(1), true);
-  chol(lch, inv, s, ny, err);
-  chol_solve(kt, lch, inv, hc, ny, nx);  // K^T = S^-1 H C
-  gemm(v, st.H(), false, st.b(), false, ny, nx, 1, st.y().p, 1, S(-1));
+  WM<S> hc = st.T(0), ha = st.T(4);
+  WM<S> v = st.t(0);
+  // [S | H C | H A | v] (<= 16 x 49, slots T1..T3) -> S^-1 [H C | H A | v]
+  const int w = ny + 2 * nx + 1;
+  WM<S> aug{st.T(1).p, w};
+  WM<S> kt{aug.p + ny, w}, wm{aug.p + ny + nx, w}, sv{aug.p + ny + 2 * nx, w};
+  gemm<false, false>(hc, st.H(), st.C(), ny, nx, nx);
+  gemm<false, false>(ha, st.H(), st.A(), ny, nx, nx);
+  gemm<false, false>(v, st.H(), st.b(), ny, nx, 1, st.y().p, 1, S(-1));
   vadd(v, v, st.d(), ny, S(-1));
-  gemm(ha, st.H(), false, st.A(), false, ny, nx, nx);
-  chol_solve(w, lch, inv, ha, ny, nx);  // S^-1 H A
-  chol_solve(sv, lch, inv, v, ny, 1);   // S^-1 v
-  gemm(st.eta(), ha, true, sv, false, nx, ny, 1, st.eta().p, 1);
-  gemm(st.J(), ha, true, w, false, nx, ny, nx, st.J().p, kLd, S(1), true);
-  gemm(st.A(), kt, true, ha, false, nx, ny, nx, st.A().p, kLd, S(-1));
-  gemm(st.b(), kt, true, v, false, nx, ny, 1, st.b().p, 1);
-  gemm(st.C(), kt, true, hc, false, nx, ny, nx, st.C().p, kLd, S(-1), true);
+  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, kLd, S(1), true);
+  copy(kt, hc, ny, nx);
+  copy(wm, ha, ny, nx);
+  copy(sv, v, ny, 1);
+  gauss_jordan(aug, ny, w, false, err);  // kt = K^T, wm = S^-1 H A, sv = S^-1 v
+  gemm<true, false>(st.eta(), ha, sv, nx, ny, 1, st.eta().p, 1);
+  gemm<true, false>(st.J(), ha, wm, nx, ny, nx, st.J().p, kLd, S(1), true);
+  gemm<true, false>(st.A(), kt, ha, nx, ny, nx, st.A().p, kLd, S(-1));
+  gemm<true, false>(st.b(), kt, v, nx, ny, 1, st.b().p, 1);
+  gemm<true, false>(st.C(), kt, hc, nx, ny, nx, st.C().p, kLd, S(-1), true);
 }
 
 // ---- kernels ----------------------------------------------------------------
@@ -291,12 +300,12 @@ __global__ void __launch_bounds__(32 * kWarps)
   for (long long k = k0; k < k1; ++k) {
     st.load(m, k);
     // predict the conditional: (F A, F b + u, F C F^T + Q)
-    gemm(st.T(6), st.F(), false, st.A(), false, nx, nx, nx);
+    gemm<false, false>(st.T(6), st.F(), st.A(), nx, nx, nx);
     copy(st.A(), st.T(6), nx, nx);
-    gemm(st.t(2), st.F(), false, st.b(), false, nx, nx, 1, st.u().p, 1);
+    gemm<false, false>(st.t(2), st.F(), st.b(), nx, nx, 1, st.u().p, 1);
     copy(st.b(), st.t(2), nx, 1);
-    gemm(st.T(6), st.F(), false, st.C(), false, nx, nx, nx);
-    gemm(st.C(), st.T(6), false, st.F(), true, nx, nx, nx, st.Q().p, kLd, S(1), true);
+    gemm<false, false>(st.T(6), st.F(), st.C(), nx, nx, nx);
+    gemm<false, true>(st.C(), st.T(6), st.F(), nx, nx, nx, st.Q().p, kLd, S(1), true);
     cond_update(st, e);
   }
   const FOffs F(nx);
@@ -316,16 +325,16 @@ __global__ void __launch_bounds__(32 * kWarps)
 template <typename S>
 __device__ void smoother_elem_pred(const Step<S>& st, unsigned& err) {
   const int n = st.nx;
-  WM<S> fp = st.T(0), pp = st.T(1), lch = st.T(2), et = st.T(3);
-  S* inv = st.t(5).p;
-  chol(lch, inv, pp, n, err);
-  chol_solve(et, lch, inv, fp, n, n);
-  for (int idx = lane_id(); idx < n * n; idx += 32) {
-    const int r = idx / n, c = idx % n;
-    st.T(4)(r, c) = et(c, r);
-  }
-  gemm(st.t(3), et, true, st.t(2), false, n, n, 1, st.b().p, 1, S(-1));
-  gemm(st.T(5), et, true, fp, false, n, n, n, st.C().p, kLd, S(-1), true);
+  WM<S> fp = st.T(0), pp = st.T(1);
+  // [pp | fp] (slots T2..T3) -> [I | pp^-1 fp] = [I | E^T]
+  WM<S> aug{st.T(2).p, 2 * n};
+  copy(aug, pp, n, n);
+  copy(WM<S>{aug.p + n, 2 * n}, fp, n, n);
+  gauss_jordan(aug, n, 2 * n, false, err);
+  const WM<S> et{aug.p + n, 2 * n};
+  for_each(n, n, [&](int r, int c) { st.T(4)(r, c) = et(c, r); });
+  gemm<true, false>(st.t(3), et, st.t(2), n, n, 1, st.b().p, 1, S(-1));
+  gemm<true, false>(st.T(5), et, fp, n, n, n, st.C().p, kLd, S(-1), true);
 }
 // Terminal element a_T = (0, x_T, P_T) (kalman_elems.hpp:158-163) into the
 // same slots.
@@ -352,35 +361,39 @@ __device__ void store_and_fold(const Step<S>& st, S* out, bool first) {
     return;
   }
   // L_a' = E_a L_k E_a^T + L_a ; g_a' = E_a g_k + g_a ; E_a' = E_a E_k
-  gemm(st.T(2), st.A(), false, st.T(5), false, n, n, n);
-  gemm(st.J(), st.T(2), false, st.A(), true, n, n, n, st.J().p, kLd, S(1), true);
-  gemm(st.t(4), st.A(), false, st.t(3), false, n, n, 1, st.t(4).p, 1);
-  gemm(st.T(6), st.A(), false, st.T(4), false, n, n, n);
+  gemm<false, false>(st.T(2), st.A(), st.T(5), n, n, n);
+  gemm<false, true>(st.J(), st.T(2), st.A(), n, n, n, st.J().p, kLd, S(1), true);
+  gemm<false, false>(st.t(4), st.A(), st.t(3), n, n, 1, st.t(4).p, 1);
+  gemm<false, false>(st.T(6), st.A(), st.T(4), n, n, n);
   copy(st.A(), st.T(6), n, n);
 }
 // Measurement update of the state (b, C) = (x, P) (kalman_seq.hpp:58-99)
 template <typename S>
 __device__ void kf_update(const Step<S>& st, unsigned& err) {
   const int nx = st.nx, ny = st.ny;
-  WM<S> hc = st.T(2), s = st.T(3), lch = st.T(4), kt = st.T(6);
+  WM<S> hc = st.T(2);
   WM<S> v = st.t(0);
-  S* inv = st.t(6).p;
-  gemm(hc, st.H(), false, st.C(), false, ny, nx, nx);
-  gemm(s, hc, false, st.H(), true, ny, nx, ny, st.R().p, kLd, S(1), true);
-  chol(lch, inv, s, ny, err);
-  chol_solve(kt, lch, inv, hc, ny, nx);
-  gemm(v, st.H(), false, st.b(), false, ny, nx, 1, st.y().p, 1, S(-1));
+  // [S | H P | v] (<= 16 x 33, slots T3..T4) -> [I | K^T | S^-1 v]
+  const int w = ny + nx + 1;
+  WM<S> aug{st.T(3).p, w};
+  WM<S> kt{aug.p + ny, w}, sv{aug.p + ny + nx, w};
+  gemm<false, false>(hc, st.H(), st.C(), ny, nx, nx);
+  gemm<false, false>(v, st.H(), st.b(), ny, nx, 1, st.y().p, 1, S(-1));
   vadd(v, v, st.d(), ny, S(-1));
-  gemm(st.b(), kt, true, v, false, nx, ny, 1, st.b().p, 1);
-  gemm(st.C(), kt, true, hc, false, nx, ny, nx, st.C().p, kLd, S(-1), true);
+  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, kLd, S(1), true);
+  copy(kt, hc, ny, nx);
+  copy(sv, v, ny, 1);
+  gauss_jordan(aug, ny, w, false, err);
+  gemm<true, false>(st.b(), kt, v, nx, ny, 1, st.b().p, 1);
+  gemm<true, false>(st.C(), kt, hc, nx, ny, nx, st.C().p, kLd, S(-1), true);
 }
 // shared prediction from (b, C) with F, Q, u in their slots
 template <typename S>
 __device__ void predict(const Step<S>& st) {
   const int n = st.nx;
-  gemm(st.T(0), st.F(), false, st.C(), false, n, n, n);
-  gemm(st.T(1), st.T(0), false, st.F(), true, n, n, n, st.Q().p, kLd, S(1), true);
-  gemm(st.t(2), st.F(), false, st.b(), false, n, n, 1, st.u().p, 1);
+  gemm<false, false>(st.T(0), st.F(), st.C(), n, n, n);
+  gemm<false, true>(st.T(1), st.T(0), st.F(), n, n, n, st.Q().p, kLd, S(1), true);
+  gemm<false, false>(st.t(2), st.F(), st.b(), n, n, 1, st.u().p, 1);
 }
 
 // finish: filter the chunk from the carried prefix.  SMOOTH = false writes
@@ -418,18 +431,23 @@ __global__ void __launch_bounds__(32 * kWarps)
     __syncwarp();
     WM<S> Ae{el + FO.A, nx}, be{el + FO.b, 1}, Ce{el + FO.C, nx}, etae{el + FO.eta, 1},
         Je{el + FO.J, nx};
-    WM<S> lu_m = st.T(3), t1 = st.T(4), t2 = st.T(5);
-    S* inv = st.t(5).p;
-    int* piv = st.sc.piv();
-    gemm(lu_m, st.C(), false, Je, false, nx, nx, nx);
-    add_eye(lu_m, nx);
-    lu(lu_m, inv, piv, nx, e);
-    gemm(st.t(1), st.C(), false, etae, false, nx, nx, 1, st.b().p, 1);
-    lu_solve(st.t(2), lu_m, inv, piv, st.t(1), nx, 1, false);
-    lu_solve(t1, lu_m, inv, piv, st.C(), nx, nx, false);
-    gemm(st.b(), Ae, false, st.t(2), false, nx, nx, 1, be.p, 1);
-    gemm(t2, Ae, false, t1, false, nx, nx, nx);
-    gemm(st.C(), t2, false, Ae, true, nx, nx, nx, Ce.p, nx, S(1), true);
+    // [M | I] (slots T3..T4) -> [I | M^-1]
+    WM<S> aug{st.T(3).p, 2 * nx};
+    WM<S> t1 = st.T(5), t2 = st.T(6);
+    gemm<false, false>(aug, st.C(), Je, nx, nx, nx);
+    for_each(nx, nx, [&](int i, int j) {
+      aug(i, nx + j) = i == j ? S(1) : S(0);
+      if (i == j) aug(i, i) += S(1);
+    });
+    __syncwarp();
+    gauss_jordan(aug, nx, 2 * nx, true, e);
+    const WM<S> Mi{aug.p + nx, 2 * nx};
+    gemm<false, false>(st.t(1), st.C(), etae, nx, nx, 1, st.b().p, 1);
+    gemm<false, false>(st.t(2), Mi, st.t(1), nx, nx, 1);
+    gemm<false, false>(t1, Mi, st.C(), nx, nx, nx);
+    gemm<false, false>(st.b(), Ae, st.t(2), nx, nx, 1, be.p, 1);
+    gemm<false, false>(t2, Ae, t1, nx, nx, nx);
+    gemm<false, true>(st.C(), t2, Ae, nx, nx, nx, Ce.p, nx, S(1), true);
   }
   for (long long k = k0; k < k1; ++k) {
     st.load(m, k);
@@ -493,9 +511,9 @@ __global__ void __launch_bounds__(32 * kWarps)
       gload(st.t(1), carry, n, 1);
       gload(st.T(1), carry + n, n, n);
       __syncwarp();
-      gemm(gs, st.T(0), false, st.t(1), false, n, n, 1, gs.p, 1);
-      gemm(st.T(2), st.T(0), false, st.T(1), false, n, n, n);
-      gemm(Ls, st.T(2), false, st.T(0), true, n, n, n, Ls.p, kLd, S(1), true);
+      gemm<false, false>(gs, st.T(0), st.t(1), n, n, 1, gs.p, 1);
+      gemm<false, false>(st.T(2), st.T(0), st.T(1), n, n, n);
+      gemm<false, true>(Ls, st.T(2), st.T(0), n, n, n, Ls.p, kLd, S(1), true);
     }
   } else {
     if (carry != nullptr) {
@@ -513,10 +531,10 @@ __global__ void __launch_bounds__(32 * kWarps)
     gload(st.t(1), ek + SO.g, n, 1);
     gload(st.T(1), ek + SO.L, n, n);
     __syncwarp();
-    gemm(st.t(2), st.T(0), false, gs, false, n, n, 1, st.t(1).p, 1);
+    gemm<false, false>(st.t(2), st.T(0), gs, n, n, 1, st.t(1).p, 1);
     copy(gs, st.t(2), n, 1);
-    gemm(st.T(2), st.T(0), false, Ls, false, n, n, n);
-    gemm(Ls, st.T(2), false, st.T(0), true, n, n, n, st.T(1).p, kLd, S(1), true);
+    gemm<false, false>(st.T(2), st.T(0), Ls, n, n, n);
+    gemm<false, true>(Ls, st.T(2), st.T(0), n, n, n, st.T(1).p, kLd, S(1), true);
     gstore(mean + i * n, gs, n, 1);
     gstore(cov + i * n * n, Ls, n, n);
     __syncwarp();
