@@ -130,7 +130,8 @@ cudaError_t repitch(void* dst, size_t dpitch, const void* src, size_t spitch, si
 // when 16-byte aligned, host (or misaligned) inputs are packed into dense
 // device arrays (time-invariant fields keep a single block, stride 0).
 template <typename S>
-int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_fuq = 0) {
+int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_fuq = 0,
+                  bool force_copy = false) {
   const long long T = (long long)m->t;
   const int nx = m->nx, ny = m->ny;
   Field f[7] = {{m->f, m->f_stride, (long long)nx * nx, "f"},
@@ -142,7 +143,9 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
                 {m->y, m->y_stride, ny, "y"}};
   const S* outp[7];
   long long outs[7];
-  const bool host = m->space == PSK_HOST;
+  // `force_copy`: device inputs that live on another GPU (two-context PTFS)
+  // are staged like host inputs; cudaMemcpyDefault resolves every pair.
+  const bool host = m->space == PSK_HOST || force_copy;
   for (int i = 0; i < 7; ++i) {
     if (!f[i].src) return fail(PSK_E_ARG, std::string("null model field ") + f[i].name);
     long long st = f[i].stride < 0 ? f[i].block : f[i].stride;
@@ -165,7 +168,7 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     const size_t pb = (bb + 15) / 16 * 16;
     S* dst = static_cast<S*>(ctx_alloc(pb * (size_t)nblk, ctx));
     if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
-    const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind kind = cudaMemcpyDefault;
     cudaError_t e = cudaSuccess;
     const size_t sp = st == 0 ? bb : sizeof(S) * (size_t)st;  // source pitch (bytes)
     if (st != 0 && pb == bb && sp == bb) {
@@ -197,7 +200,7 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
   // prior mean at [0, nx) rounded up to a 16-byte boundary, cov after it
   const int moff = (int)((sizeof(S) * nx + 15) / 16 * 16 / sizeof(S));
   S* pcov = prior + moff;
-  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind kind = cudaMemcpyDefault;
   cudaError_t e1 = cudaMemcpyAsync(prior, pm, sizeof(S) * nx, kind, ctx->stream);
   cudaError_t e2 = cudaMemcpyAsync(pcov, pc, sizeof(S) * nx * nx, kind, ctx->stream);
   if (e1 != cudaSuccess || e2 != cudaSuccess)
@@ -469,6 +472,108 @@ int fold_entry(psk_ctx* ctx, int kind, int dtype, int nx, const void* elems, int
   return finish_call(ctx, st);
 }
 
+template <typename S>
+int ptfs_two_typed(psk_ctx* cf, psk_ctx* cb, const psk_model* m, int alg, uint64_t sn,
+                   void* mean, void* cov) {
+  const long long T = (long long)m->t;
+  const int nx = m->nx;
+  ModelView<S> va, vb;
+  int st;
+  {
+    DeviceGuard dg(cb->device);
+    int dev = -1;
+    cudaPointerAttributes at{};
+    const bool foreign = m->space == PSK_DEVICE &&
+                         cudaPointerGetAttributes(&at, m->f) == cudaSuccess &&
+                         at.type == cudaMemoryTypeDevice && at.device != cb->device;
+    (void)dev;
+    st = prepare_model<S>(cb, m, vb, 0, foreign);
+    if (st) return st;
+  }
+  DeviceGuard dg(cf->device);
+  st = prepare_model<S>(cf, m, va);
+  if (st) return st;
+  const bool host = m->space == PSK_HOST;
+  const size_t mb = sizeof(S) * (size_t)T * nx, cb_ = sizeof(S) * (size_t)T * nx * nx;
+  S* dmean = static_cast<S*>(mean);
+  S* dcov = static_cast<S*>(cov);
+  const bool tmp_out = host || !aligned16(mean) || !aligned16(cov);
+  if (tmp_out) {
+    dmean = static_cast<S*>(ctx_alloc(mb + 16, cf));
+    dcov = static_cast<S*>(ctx_alloc(cb_ + 16, cf));
+    if (!dmean || !dcov) return fail(PSK_E_ALLOC, "device allocation failed (outputs)");
+  }
+  FastArgs a;
+  a.method = 2;
+  a.alg = alg;
+  a.sengupta_n = sn;
+  a.chunk = cf->chunk;
+  a.waves = cf->waves;
+  st = fast_ptfs2<S>(cf->launch, va, cf->device, cb->launch, vb, cb->device, a, dmean, dcov,
+                     ctx_alloc, cf, ctx_alloc, cb);
+  cudaSetDevice(cf->device);
+  if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
+  if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (scan)");
+  if (st) return fail(PSK_E_CUDA, "two-context PTFS failed");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+  if (tmp_out) {
+    cudaMemcpyAsync(mean, dmean, mb, cudaMemcpyDefault, cf->stream);
+    cudaMemcpyAsync(cov, dcov, cb_, cudaMemcpyDefault, cf->stream);
+  }
+  return PSK_OK;
+}
+
+int ptfs_two(psk_ctx* cf, psk_ctx* cb, const psk_model* m, int alg, uint64_t sn, void* mean,
+             void* cov) {
+  if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16) return fail(PSK_E_DIM, "mat dims");
+  if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+  if (m->space != PSK_HOST && m->space != PSK_DEVICE) return fail(PSK_E_ARG, "bad space");
+  int st = check_contract(alg, sn, m->t);
+  if (st) return st;
+  if (!mean || !cov) return fail(PSK_E_ARG, "null output");
+  // one caller at a time per context (like PoolBackend); lock in address
+  // order so two concurrent two-context calls cannot deadlock
+  psk_ctx* lo = cf < cb ? cf : cb;
+  psk_ctx* hi = cf < cb ? cb : cf;
+  std::lock_guard<std::mutex> l1(lo->mu);
+  std::lock_guard<std::mutex> l2(hi->mu);
+  for (psk_ctx* c : {cf, cb}) {
+    DeviceGuard dg(c->device);
+    c->launch.stream = c->stream;
+    c->launch.err = c->d_err;
+    c->launch.start();
+    cudaMemsetAsync(c->d_err, 0, sizeof(unsigned), c->stream);
+  }
+  st = m->dtype == PSK_F64 ? ptfs_two_typed<double>(cf, cb, m, alg, sn, mean, cov)
+                           : ptfs_two_typed<float>(cf, cb, m, alg, sn, mean, cov);
+  unsigned herr[2] = {0, 0};
+  cudaError_t e = cudaSuccess;
+  int i = 0;
+  for (psk_ctx* c : {cf, cb}) {
+    DeviceGuard dg(c->device);
+    cudaMemcpyAsync(&herr[i++], c->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream);
+    ctx_free_all(c);
+    const cudaError_t ec = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = ec;
+  }
+  if (st) return st;
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  for (psk_ctx* c : {cf, cb}) {  // per-kernel timing of each context
+    c->profile.clear();
+    if (c->launch.profile && c->launch.evs.size() > 1)
+      for (size_t k = 0; k + 1 < c->launch.evs.size(); ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->launch.evs[k], c->launch.evs[k + 1]);
+        c->profile.emplace_back(c->launch.names[k], ms);
+      }
+  }
+  const unsigned herr_all = herr[0] | herr[1];
+  if (herr_all & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr_all & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
+  return PSK_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -581,10 +686,15 @@ int psk_ptfs(psk_ctx* cf, psk_ctx* cb, int devices, const psk_model* m, int alg,
              void* mean, void* cov) {
   if (devices != 1 && devices != 2) return fail(PSK_E_ARG, "devices must be 1 or 2");
   if (!cb) cb = cf;
-  // The backward scan is independent of the forward scan; both are issued
-  // on the forward context's stream in this version (numbers are identical
-  // for any placement, test_kalman_par.cpp:209-227).
-  (void)cb;
+  // devices == 2 with a second context: forward filter on ctx_fwd and the
+  // backward reduce + scan on ctx_bwd, concurrently.
+  // Anything the split does not cover runs on the forward context alone; the
+  // numbers do not depend on the placement (test_kalman_par.cpp:209-227).
+  if (devices == 2 && cb != cf && m && cf && cf->mode == PSK_MODE_FAST &&
+      cb->mode == PSK_MODE_FAST && m->t > 0 &&
+      (m->dtype == PSK_F64 ? fast_supported<double>(m->nx, m->ny)
+                           : fast_supported<float>(m->nx, m->ny)))
+    return ptfs_two(cf, cb, m, alg, sn, mean, cov);
   return run_entry(cf, m, 2, alg, sn, mean, cov);
 }
 

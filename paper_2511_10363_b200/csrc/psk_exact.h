@@ -68,6 +68,13 @@ template <typename S>
 int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
              void* (*alloc)(size_t, void*), void* alloc_ctx);
 
+// PTFS with forward (A) and backward (B) passes on two contexts
+template <typename S>
+int fast_ptfs2(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& LB,
+               const ModelView<S>& mB, int devB, const FastArgs& a, S* mean, S* cov,
+               void* (*allocA)(size_t, void*), void* ctxA, void* (*allocB)(size_t, void*),
+               void* ctxB);
+
 template <typename S>
 int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
                      void** scratch, S* mean, S* cov, const S* carry, S* elem_out,

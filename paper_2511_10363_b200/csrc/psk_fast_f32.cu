@@ -11,6 +11,9 @@ template int fast_shard_phase<float>(ExactLaunch&, const ModelView<float>&, cons
                                   void**, float*, float*, const float*, float*,
                                   void* (*)(size_t, void*), void*);
 template void fast_shard_release<float>(void*);
+template int fast_ptfs2<float>(ExactLaunch&, const ModelView<float>&, int, ExactLaunch&,
+                            const ModelView<float>&, int, const FastArgs&, float*, float*,
+                            void* (*)(size_t, void*), void*, void* (*)(size_t, void*), void*);
 template int fast_fold<float>(ExactLaunch&, int, int, const float*, int, float*);
 template int wide::wide_run<float>(ExactLaunch&, const ModelView<float>&, const FastArgs&, float*,
                                float*, void* (*)(size_t, void*), void*);

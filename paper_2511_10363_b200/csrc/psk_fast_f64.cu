@@ -11,6 +11,9 @@ template int fast_shard_phase<double>(ExactLaunch&, const ModelView<double>&, co
                                   void**, double*, double*, const double*, double*,
                                   void* (*)(size_t, void*), void*);
 template void fast_shard_release<double>(void*);
+template int fast_ptfs2<double>(ExactLaunch&, const ModelView<double>&, int, ExactLaunch&,
+                            const ModelView<double>&, int, const FastArgs&, double*, double*,
+                            void* (*)(size_t, void*), void*, void* (*)(size_t, void*), void*);
 template int fast_fold<double>(ExactLaunch&, int, int, const double*, int, double*);
 template int wide::wide_run<double>(ExactLaunch&, const ModelView<double>&, const FastArgs&, double*,
                                double*, void* (*)(size_t, void*), void*);

@@ -240,6 +240,45 @@ static int fast_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, 
   return 0;
 }
 
+// PTFS with the forward and the backward pass on two contexts (two GPUs, or
+// two streams of one): the backward (shifted-element) reduce + reversed scan
+// runs on B concurrently with the forward filter on A; the scanned backward
+// chunk elements (nchunks x 56 scalars, not the per-step (eta, J) the
+// reference copies, kalman_par.hpp:223-236) are then copied to A, where the
+// backward finish fused with the two-filter combination writes the smoothed
+// stats.  `mA`/`mB` view the same model on each device.
+template <typename S, int NX, int NY>
+static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& LB,
+                        const ModelView<S>& mB, int devB, FastArgs a, S* mean, S* cov,
+                        void* (*allocA)(size_t, void*), void* ctxA,
+                        void* (*allocB)(size_t, void*), void* ctxB) {
+  if (mA.t == 0) return 0;
+  a.method = 2;
+  if (a.chunk < 1) a.chunk = auto_chunk<S, NX, NY>(mA.t, a.waves);  // same L on both sides
+  FastScratch<S> sa, sb;
+  cudaSetDevice(devB);
+  int st = fast_prepare_t<S, NX, NY>(mB, a, sb, allocB, ctxB);
+  if (st) return st;
+  st = fast_phase_t<S, NX, NY>(LB, mB, a, sb, 4, nullptr, nullptr, nullptr, nullptr);
+  if (st) return st;
+  cudaEvent_t done_b;
+  cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming);
+  cudaEventRecord(done_b, LB.stream);
+  cudaSetDevice(devA);
+  st = fast_prepare_t<S, NX, NY>(mA, a, sa, allocA, ctxA);
+  if (st) return st;
+  st = fast_phase_t<S, NX, NY>(LA, mA, a, sa, 0, mean, cov, nullptr, nullptr);
+  if (!st) st = fast_phase_t<S, NX, NY>(LA, mA, a, sa, 1, mean, cov, nullptr, nullptr);
+  if (st) return st;
+  // the forward elements in sa.agg are dead after the forward finish
+  cudaStreamWaitEvent(LA.stream, done_b, 0);
+  cudaMemcpyPeerAsync(sa.agg, devA, sb.agg, devB,
+                      sizeof(S) * FLayout<NX>::size * (size_t)sa.npad, LA.stream);
+  LA.count("ptfs_backward_elements_peer_copy");
+  cudaEventDestroy(done_b);
+  return fast_phase_t<S, NX, NY>(LA, mA, a, sa, 5, mean, cov, nullptr, nullptr);
+}
+
 // compiled (nx, ny) instantiations of the fast path
 #define PSK_FAST_DIMS(X) \
   X(1, 1)                \
@@ -267,6 +306,20 @@ int fast_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
              void* (*alloc)(size_t, void*), void* actx) {
 #define PSK_CASE(A, B) \
   if (m.nx == A && m.ny == B) return fast_run_t<S, A, B>(L, m, a, mean, cov, alloc, actx);
+  PSK_FAST_DIMS(PSK_CASE)
+#undef PSK_CASE
+  return -1;
+}
+
+template <typename S>
+int fast_ptfs2(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& LB,
+               const ModelView<S>& mB, int devB, const FastArgs& a, S* mean, S* cov,
+               void* (*allocA)(size_t, void*), void* ctxA, void* (*allocB)(size_t, void*),
+               void* ctxB) {
+#define PSK_CASE(A, B)                                                                      \
+  if (mA.nx == A && mA.ny == B)                                                             \
+    return fast_ptfs2_t<S, A, B>(LA, mA, devA, LB, mB, devB, a, mean, cov, allocA, ctxA, \
+                                 allocB, ctxB);
   PSK_FAST_DIMS(PSK_CASE)
 #undef PSK_CASE
   return -1;

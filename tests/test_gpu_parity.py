@@ -139,6 +139,35 @@ def test_wide_path_large_t(psk, gpu, port):
     assert max_rel_err(got.mean, got.cov, *rts) < TOL64
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ptfs_two_contexts(psk, gpu, port, dtype):
+    """devices = 2 with a second context: the backward reduce + scan runs on
+    ctx_bwd concurrently with the forward filter on ctx_fwd (PAPER.md:885-890);
+    the result is bitwise the single-context PTFS (test_kalman_par.cpp:
+    209-227: devices 1 and 2 bitwise equal) and within the gate of rts_run."""
+    import torch
+    fwd = psk.CudaBackend(gpu, mode="fast")
+    bwd = psk.CudaBackend(gpu, mode="fast")
+    m, ys = gen(port, 41, 4, 2, 3000)
+    if dtype == np.float32:
+        m, ys = _cast(m, ys, np.float32)
+    for alg in (6, 3):
+        spec = psk.ScanSpec(psk.ScanAlg(alg), 4)
+        one = psk.ptfs_run(m, ys, spec, fwd)
+        two = psk.ptfs_run(m, ys, spec, fwd, bwd, 2)
+        assert np.array_equal(one.mean, two.mean) and np.array_equal(one.cov, two.cov)
+    if dtype == np.float64:
+        rts = port.rts_run(m, ys)
+        assert max_rel_err(two.mean, two.cov, *rts) < TOL64
+        # device-resident inputs
+        t = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+        md = psk.Lgssm(f=t(m.f), u=t(m.u), q=t(m.q), h=t(m.h), d=t(m.d), r=t(m.r),
+                       prior_mean=t(m.prior_mean), prior_cov=t(m.prior_cov), t=m.t)
+        spec6 = psk.ScanSpec(psk.ScanAlg(6))
+        dev = psk.ptfs_run(md, t(ys), spec6, fwd, bwd, 2)
+        assert np.array_equal(_np(dev.mean), psk.ptfs_run(m, ys, spec6, fwd, bwd, 2).mean)
+
+
 def test_fast_many_seeds_acceptance(psk, fast, port):
     """acceptance criterion 3 shape (test_acceptance.cpp:102-127)."""
     for seed in range(10):
