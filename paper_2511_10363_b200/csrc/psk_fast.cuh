@@ -98,6 +98,40 @@ __device__ __forceinline__ SElem<S, NX> egl_load(const S* p, long long cap) {
   return e;
 }
 
+// Per-step filtered states (x, upper P) handed from the PTFS forward finish to
+// the backward finish in the same chunk-interleaved layout as the smoothing
+// elements (index (j * size + comp) * cap + chunk: coalesced both ways).
+template <int NX>
+struct StateLayout {
+  static constexpr int x = 0, P = NX, size = NX + NX * (NX + 1) / 2;
+};
+template <typename S, int NX>
+__device__ __forceinline__ void state_store(S* p, long long cap, const Vec<S, NX>& x,
+                                            const Mat<S, NX, NX>& P) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) __stcs(p + i * cap, x.a[i][0]);
+  int q = NX;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) __stcs(p + (q++) * cap, P.a[i][j]);
+}
+template <typename S, int NX>
+__device__ __forceinline__ void state_load(const S* p, long long cap, Vec<S, NX>& x,
+                                           Mat<S, NX, NX>& P) {
+#pragma unroll
+  for (int i = 0; i < NX; ++i) x.a[i][0] = __ldcs(p + i * cap);
+  int q = NX;
+#pragma unroll
+  for (int i = 0; i < NX; ++i)
+#pragma unroll
+    for (int j = i; j < NX; ++j) {
+      const S v = __ldcs(p + (q++) * cap);
+      P.a[i][j] = v;
+      P.a[j][i] = v;
+    }
+}
+
 template <typename S, int NX>
 __device__ __forceinline__ FElem<S, NX> fe_load(const S* p, long long cap,
                                                 long long i) {
@@ -529,6 +563,56 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
   }
 }
 
+// The same double-buffered TMA walk, backwards: positions j = jn-1 .. 0 of
+// the chunk (body(k0 + j, stage) for the thread's positions inside [k0, k1);
+// `valid` positions are those < m.t, the others see no data).  `jn` is the
+// CTA-uniform walk length chosen by the caller.
+template <typename S, int NX, int NY, class Body>
+__device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const StageMaps& maps,
+                                                const ModelView<S>& m, long long L,
+                                                long long nfull, long long jn, long long k0,
+                                                long long k1, Body&& body) {
+  using In = FilterTma<S, NX, NY>;
+  using St = FilterStage<S, NX, NY>;
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * In::stage);
+  const int t = threadIdx.x;
+  const long long cta0 = (long long)blockIdx.x * kStageNT;
+  const bool tma = cta0 < nfull;
+  const bool direct = !tma || cta0 + t >= nfull;
+  // positions >= the m-length of the CTA's first chunk carry no data
+  const long long jd = min(jn, max(0LL, m.t - cta0 * L));
+  auto issue = [&](int s, long long j) {
+    fence_proxy_async();
+    mbar_expect_tx(&bars[s], maps.tx);
+#pragma unroll
+    for (int f = 0; f < 7; ++f)
+      if (maps.use[f])
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j, (int)cta0, &bars[s]);
+  };
+  if (tma && t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+    if (jd > 0) issue(0, jd - 1);
+  }
+  __syncthreads();
+  long long it = 0;  // fetches consumed so far
+  for (long long j = jn - 1; j >= 0; --j) {
+    const bool data = j < jd;
+    const int s = (int)(it & 1);
+    if (data) {
+      if (tma && t == 0 && j >= 1) issue(s ^ 1, j - 1);
+      if (tma) mbar_wait(&bars[s], (unsigned)((it >> 1) & 1));
+    }
+    const long long k = k0 + j;
+    if (k < k1) body(k, k < m.t, St{sm + s * In::stage, t, direct, &m, k});
+    __syncthreads();
+    if (data) ++it;
+  }
+}
+
 // Filtering element of step k from its staged inputs (make_filter_element,
 // kalman_elems.hpp:97-147, k > 1)
 template <typename S, int NX, int NY>
@@ -677,7 +761,9 @@ __device__ __forceinline__ SElem<S, NX> smoother_elem_pred(const Vec<S, NX>& x,
 }
 
 // finish: sequential Kalman filter over the chunk from the carried prefix.
-// SMOOTH = false (PKF, PTFS): writes the filtered stats.  SMOOTH = true
+// SMOOTH = false: writes the filtered stats -- to mean/cov (PKF), or, when
+// `egl` is non-null (PTFS), coalesced to the chunk-interleaved state scratch
+// the backward finish reads (StateLayout).  SMOOTH = true
 // (PRTS): the caller needs the smoothed stats only, so the pass writes the
 // per-step smoothing elements e_k instead and folds the chunk's smoothing
 // element e_{k0} (x) ... (x) e_{k1-1} into `sagg` (Lemma 2 is associative,
@@ -733,7 +819,12 @@ __global__ void __launch_bounds__(kStageNT, 2)
     x = xp;
     P = pp;
     kf_update(x, P, in.meas(), e);
-    if constexpr (!SMOOTH) store_state(mean, cov, k, x, P);
+    if constexpr (!SMOOTH) {
+      if (egl == nullptr)
+        store_state(mean, cov, k, x, P);
+      else
+        state_store(egl + (k - k0) * StateLayout<NX>::size * ecap + c, ecap, x, P);
+    }
   });
   if constexpr (SMOOTH) {
     if (live) {  // element of the chunk's last step
@@ -884,57 +975,44 @@ __global__ void __launch_bounds__(kSmoothNT)
 // Two-filter smoother: backward (shifted) filter + combination (K8)
 // ============================================================================
 
-// reduce: slots [k0, k1) hold a_{i+2} (0-based step i+1) or the identity
-// (build_shifted_filter_elems, kalman_par.hpp:63-89); the chunk element is
-// their ordered product.
-template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(128)
-    k_bwd_reduce(ModelView<S> m, long long L, long long nchunks, S* agg,
-                 long long cap, unsigned* err) {
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  unsigned e = 0;
-  const long long k0 = c * L;
-  const long long k1 = min(k0 + L, m.t);
-  // slots with i + 1 <= T - 1 carry an element
-  const long long last = min(k1, m.last_step);  // exclusive end of real slots
-  FElem<S, NX> a;
-  if (last <= k0) {
-    a = fe_identity<S, NX>();
-  } else {
-    a = make_filter_elem<S, NX, NY>(m, last, e);  // slot last-1 -> step last
-    for (long long i = last - 2; i >= k0; --i) {
-      const FElem<S, NX> ei = make_filter_elem<S, NX, NY>(m, i + 1, e);
-      a = filter_combine(ei, a, e);
-    }
-  }
-  fe_store(agg, cap, c, a);
-  if (e) atomicOr(err, e);
-}
-
 // finish: backward information recursion (eta, J) <- a (x) (eta, J) over the
-// chunk, fused with tf_combine (kalman_seq.hpp:236-260) against the filtered
-// stats held in mean/cov (overwritten in place with the smoothed stats).
+// chunk's slots, walking backwards, fused with tf_combine (kalman_seq.hpp:
+// 236-260) against the filtered states of the forward finish (state scratch),
+// writing the smoothed stats to mean/cov.  Slot i holds a_{i+2} (1-based; the element of 0-based
+// step i+1) or the identity (build_shifted_filter_elems, kalman_par.hpp:
+// 63-89); `ms` is the model shifted by one step (ms step i = m step i+1,
+// ms.t = T - 1), staged by TMA like the forward passes.
 template <typename S, int NX, int NY>
-__global__ void __launch_bounds__(128)
-    k_bwd_finish(ModelView<S> m, long long L, long long nchunks, const S* suf,
-                 long long suf_cap, S* mean, S* cov, unsigned* err) {
+__global__ void __launch_bounds__(kStageNT, 2)
+    k_bwd_finish(ModelView<S> ms, const __grid_constant__ StageMaps maps, long long T,
+                 long long L, long long nchunks, long long nfull, const S* suf, long long suf_cap,
+                 const S* fst, long long fcap, S* mean, S* cov, unsigned* err) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
+  using St = FilterStage<S, NX, NY>;
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
+  const bool live = c < nchunks;
   unsigned e = 0;
   const long long k0 = c * L;
-  const long long k1 = min(k0 + L, m.t);
+  const long long k1 = min(k0 + L, T);
+  const long long cta0 = (long long)blockIdx.x * kStageNT;
+  const long long jn = min(L, T - cta0 * L);  // CTA-uniform (slots of the CTA's first chunk)
   Vec<S, NX> eta = zeros<S, NX, 1>();
   Mat<S, NX, NX> J = zeros<S, NX, NX>();
-  if (c + 1 < nchunks) {
+  if (live && c + 1 < nchunks) {
     eta = load_soa<S, NX, 1>(suf + FLayout<NX>::eta * suf_cap + (c + 1), suf_cap);
     J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + (c + 1), suf_cap);
   }
-  for (long long i = k1 - 1; i >= k0; --i) {
-    if (i + 1 <= m.last_step) {
-      // (eta, J) of a (x) s for the element a of step i+1 (Lemma 1, eta/J
+  staged_walk_rev<S, NX, NY>(fsm, maps, ms, L, nfull, jn, k0, k1,
+                             [&](long long i, bool has, const St& in) {
+    if (has) {
+      // (eta, J) of a (x) s for the element a of ms step i (Lemma 1, eta / J
       // rows only: they depend on the right operand through (eta, J) alone)
-      const FElem<S, NX> a = make_filter_elem<S, NX, NY>(m, i + 1, e);
+      FElem<S, NX> a = fe_identity<S, NX>();
+      const Mat<S, NX, NX> F = in.F();
+      a.A = F;
+      a.b = in.u();
+      a.C = in.Q();
+      cond_update(a, in.meas(), e);
       Mat<S, NX, NX> nm = mul(J, a.C);  // N = I + J_s C_a
 #pragma unroll
       for (int q = 0; q < NX; ++q) nm.a[q][q] += S(1);
@@ -949,7 +1027,7 @@ __global__ void __launch_bounds__(128)
     // two-filter combination: (I + P J)^-1 (x + P eta), (I + P J)^-1 P
     Vec<S, NX> x;
     Mat<S, NX, NX> P;
-    load_state(mean, cov, i, x, P);
+    state_load(fst + (i - k0) * StateLayout<NX>::size * fcap + c, fcap, x, P);
     Mat<S, NX, NX> mm = mul(P, J);
 #pragma unroll
     for (int q = 0; q < NX; ++q) mm.a[q][q] += S(1);
@@ -959,7 +1037,7 @@ __global__ void __launch_bounds__(128)
     Mat<S, NX, NX> ps = lu_solve(lu, P);
     symmetrize(ps);
     store_state(mean, cov, i, xs, ps);
-  }
+  });
   if (e) atomicOr(err, e);
 }
 

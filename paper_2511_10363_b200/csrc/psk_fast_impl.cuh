@@ -26,6 +26,25 @@ inline int grid_for(long long n, int block) {
 constexpr int kBlock = 128;
 }  // namespace
 
+// The model shifted by one step (step i of the view = step i + 1 of m,
+// t - 1 steps, no prior): the backward pass of PTFS walks the elements
+// a(step i+1) at slot i.
+template <typename S>
+ModelView<S> shift_model(const ModelView<S>& m) {
+  ModelView<S> v = m;
+  v.f += m.sf;
+  v.u += m.su;
+  v.q += m.sq;
+  v.h += m.sh;
+  v.d += m.sd;
+  v.r += m.sr;
+  v.y += m.sy;
+  v.t = m.t > 0 ? m.t - 1 : 0;
+  v.prior_first = 0;
+  v.last_step = v.t - 1;
+  return v;
+}
+
 // Scan of chunk elements: level-by-level plan (alg 0..5) or the single-pass
 // decoupled look-back (alg 6).  `buf` holds npad slots (identity padded).
 template <class Ops>
@@ -103,9 +122,11 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
   sc.sagg = (S*)alloc(sizeof(S) * SLayout<NX>::size * (sc.npad ? sc.npad : 1), actx);
   sc.sagg_valid = false;
   sc.egl = nullptr;
-  if (a.method == 1) {
-    sc.ecap = (sc.nchunks + 31) / 32 * 32;
-    sc.egl = (S*)alloc(sizeof(S) * (size_t)EglLayout<NX>::size * (size_t)sc.chunk *
+  sc.ecap = (sc.nchunks + 31) / 32 * 32;
+  if (a.method == 1 || a.method == 2) {
+    // PRTS: per-step smoothing elements; PTFS: per-step filtered states
+    const int per = a.method == 1 ? EglLayout<NX>::size : StateLayout<NX>::size;
+    sc.egl = (S*)alloc(sizeof(S) * (size_t)per * (size_t)sc.chunk *
                            (size_t)(sc.ecap ? sc.ecap : 32),
                        actx);
     if (!sc.egl) return 8;
@@ -131,7 +152,6 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
   const long long Lc = sc.chunk, nch = sc.nchunks, npad = sc.npad;
   FastFilterOps<S, NX> fops{L.err};
   FastSmootherOps<S, NX> sops{L.err};
-  const int g = blocks_for(nch, kBlock);
   auto fill = [&](auto ops, S* buf) {
     if (npad > nch) {
       k_fill_identity<<<blocks_for(npad - nch, kBlock), kBlock, 0, L.stream>>>(
@@ -174,8 +194,8 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
         cudaFuncSetAttribute(k_filter_finish<S, NX, NY, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
         k_filter_finish<S, NX, NY, false><<<gs, kStageNT, stage_bytes, L.stream>>>(
-            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad, nullptr,
-            sc.ecap, L.err);
+            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad,
+            a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
         L.count("filter_finish");
       }
       sc.sagg_valid = a.method == 1;
@@ -206,17 +226,43 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       L.count("smoother_finish");
       sc.sagg_valid = false;
       break;
-    case 4:
-      k_bwd_reduce<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, L.err);
-      L.count("bwd_reduce");
-      fill(fops, sc.agg);
+    case 4: {
+      // backward elements: slot i = a(step i+1) -> the filter reduce over the
+      // model shifted by one step (chunk c of it = slots [cL, cL + L)), from
+      // the identity; chunks past T - 1 steps are pure identity
+      const ModelView<S> ms = shift_model(m);
+      const long long nch_s = ms.t > 0 ? (ms.t + Lc - 1) / Lc : 0;
+      StageMaps smaps;
+      const int st = make_stage_maps<S, NX, NY>(ms, Lc, ms.t / Lc, smaps);
+      if (st) return st;
+      if (nch_s > 0) {
+        cudaFuncSetAttribute(k_filter_reduce<S, NX, NY>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        k_filter_reduce<S, NX, NY><<<blocks_for(nch_s, kStageNT), kStageNT, stage_bytes,
+                                     L.stream>>>(ms, smaps, Lc, nch_s, ms.t / Lc, sc.agg, npad,
+                                                 L.err);
+        L.count("bwd_reduce");
+      }
+      if (npad > nch_s) {
+        k_fill_identity<<<blocks_for(npad - nch_s, kBlock), kBlock, 0, L.stream>>>(
+            fops, ElemBuf<S>{sc.agg, npad, npad, 0}, nch_s, npad);
+        L.count("fill_identity");
+      }
       chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
       break;
-    case 5:
-      k_bwd_finish<S, NX, NY><<<g, kBlock, 0, L.stream>>>(m, Lc, nch, sc.agg, npad, mean, cov,
-                                                          L.err);
+    }
+    case 5: {
+      const ModelView<S> ms = shift_model(m);
+      StageMaps smaps;
+      const int st = make_stage_maps<S, NX, NY>(ms, Lc, ms.t / Lc, smaps);
+      if (st) return st;
+      cudaFuncSetAttribute(k_bwd_finish<S, NX, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           stage_bytes);
+      k_bwd_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
+          ms, smaps, m.t, Lc, nch, ms.t / Lc, sc.agg, npad, sc.egl, sc.ecap, mean, cov, L.err);
       L.count("bwd_finish_tf_combine");
       break;
+    }
     default:
       return 7;
   }
