@@ -102,6 +102,9 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
  *   "chunk"     steps folded per thread, 0 = auto (same as psk_set_chunk)
  *   "waves"     auto chunk: the chunks fill this many waves of co-resident
  *               threads (default 4)
+ *   "shard_async"  1: the shard phases before psk_shard_smoother_finish and
+ *               the folds return without synchronising the stream (errors
+ *               are reported by the smoother finish); default 0
  * Returns PSK_E_ARG for an unknown key or value. */
 int psk_set_option(psk_ctx* ctx, const char* key, int64_t value);
 /* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).

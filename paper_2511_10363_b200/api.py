@@ -191,8 +191,15 @@ class CudaBackend:
         self.chunk = int(chunk)
 
     def set_stream(self, stream: Any) -> None:
-        handle = getattr(stream, "cuda_stream", stream)
-        _check(_lib.lib().psk_set_stream(self._ctx, C.c_void_p(handle or 0)))
+        """Run on `stream` (a torch.cuda.Stream or a raw cudaStream_t); None
+        restores the context's own stream.  torch's default stream is the
+        legacy NULL stream, passed as cudaStreamLegacy (handle 1): a NULL
+        handle means "own stream" to the C-ABI."""
+        if stream is None:
+            handle = 0
+        else:
+            handle = getattr(stream, "cuda_stream", stream) or 1
+        _check(_lib.lib().psk_set_stream(self._ctx, C.c_void_p(handle)))
 
     def set_profile(self, on: bool) -> None:
         _check(_lib.lib().psk_set_profile(self._ctx, int(bool(on))))

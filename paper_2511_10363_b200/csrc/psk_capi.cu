@@ -39,6 +39,7 @@ struct psk_ctx {
   int mode = PSK_MODE_FAST;
   long long chunk = 0;  // 0: auto (whole waves of chunks)
   int waves = 4;        // waves of chunks for the auto chunk length
+  int shard_async = 0;  // shard phases 0-2 and folds return without a host sync
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
@@ -444,10 +445,23 @@ int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   ctx->launch.stream = ctx->stream;
   ctx->launch.err = ctx->d_err;
   ctx->launch.start();
-  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  // "shard_async": the phases before the smoother finish return without a
+  // host synchronisation (the error word accumulates and is checked by the
+  // final phase), so a rank's phases and its NCCL exchanges stay queued on
+  // the stream back to back
+  const bool defer = ctx->shard_async && phase != 3;
+  if (!ctx->shard_async || phase == 0)
+    cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   int st = m->dtype == PSK_F64
                ? shard_typed<double>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out)
                : shard_typed<float>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out);
+  if (defer) {
+    ctx_free_all(ctx);
+    if (st) return st;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+    return PSK_OK;
+  }
   return finish_call(ctx, st);
 }
 
@@ -462,13 +476,19 @@ int fold_entry(psk_ctx* ctx, int kind, int dtype, int nx, const void* elems, int
   ctx->launch.stream = ctx->stream;
   ctx->launch.err = ctx->d_err;
   ctx->launch.start();
-  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  if (!ctx->shard_async) cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   int st = dtype == PSK_F64
                ? fast_fold<double>(ctx->launch, kind, nx, static_cast<const double*>(elems),
                                    count, static_cast<double*>(out))
                : fast_fold<float>(ctx->launch, kind, nx, static_cast<const float*>(elems),
                                   count, static_cast<float*>(out));
   if (st) st = fail(PSK_E_ARG, "fold failed");
+  if (ctx->shard_async) {  // see shard_entry
+    if (st) return st;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+    return PSK_OK;
+  }
   return finish_call(ctx, st);
 }
 
@@ -643,6 +663,9 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   if (k == "chunk") {
     if (value < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
     c->chunk = value;
+  } else if (k == "shard_async") {
+    if (value != 0 && value != 1) return fail(PSK_E_ARG, "shard_async must be 0 or 1");
+    c->shard_async = (int)value;
   } else if (k == "waves") {
     if (value < 1 || value > 1024) return fail(PSK_E_ARG, "waves must be 1..1024");
     c->waves = (int)value;

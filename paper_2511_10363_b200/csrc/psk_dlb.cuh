@@ -271,13 +271,8 @@ void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf,
   using S = typename Ops::S;
   if (n <= 0) return;
   const size_t smem = sizeof(S) * (size_t)Ops::kSize * kDlbSlots;
-  // the attribute is per device: set it on every call (cheap)
-  cudaFuncSetAttribute(k_dlb<Ops>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dlb<Ops>, kDlbThreads, smem);
-  const int per = dlb_per_thread(n, (long long)sms * per_sm);
+  const int per_sm = kernel_setup(k_dlb<Ops>, kDlbThreads, (int)smem);
+  const int per = dlb_per_thread(n, (long long)device_sms() * per_sm);
   const long long ntiles = dlb_tiles(n, per);
   cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
   static unsigned long long* trace = nullptr;  // PSK_DLB_TRACE: stamps of the last scan

@@ -2,12 +2,49 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "psk_common.cuh"
 #include "psk_plan.hpp"
 
 namespace psk {
+
+// Per-device, per-kernel launch setup, done once: raise the kernel's dynamic
+// shared-memory limit to `smem` and return its co-resident CTAs per SM
+// (cudaFuncSetAttribute / the occupancy query cost microseconds per call,
+// which showed as idle gaps between the short kernels of a small-T run).
+template <class Kernel>
+int kernel_setup(Kernel kernel, int block, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, block, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+  cache[key] = per_sm;
+  return per_sm;
+}
+inline int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] = sms > 0 ? sms : 148;
+}
 
 // Launch bookkeeping shared by all paths: the stream, the device error word,
 // a launch counter and optional per-kernel CUDA-event timing.

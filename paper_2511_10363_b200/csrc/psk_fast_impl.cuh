@@ -74,21 +74,20 @@ static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
 // folds ceil(chunks / resident) per thread), more waves keep the per-step
 // kernels closer to the HBM roof; 4 is the measured optimum at T = 2^24
 // (profiles/r01_v3: L = 64/74/111/148/222/443 -> 5.08/4.96/4.85/4.99/5.03/
-// 5.17 ms per PRTS).
+// 5.17 ms per PRTS) ...
 template <typename S, int NX, int NY>
 long long auto_chunk(long long T, int waves) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int smem = FilterTma<S, NX, NY>::smem;
-  cudaFuncSetAttribute(k_filter_finish<S, NX, NY, true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter_finish<S, NX, NY, true>,
-                                                kStageNT, smem);
-  const long long resident = (long long)(sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1) *
-                             kStageNT * (waves > 0 ? waves : 1);
-  const long long L = (T + resident - 1) / resident;
-  return L < 1 ? 1 : L;
+  const int per_sm = kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT,
+                                  FilterTma<S, NX, NY>::smem);
+  const long long wave = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kStageNT;
+  const long long L = (T + wave * (waves > 0 ? waves : 1) - 1) / (wave * (waves > 0 ? waves : 1));
+  // ... but at least 64 steps per chunk unless that leaves less than one
+  // wave of chunks: short chunks make the per-chunk costs (incoming state,
+  // chunk-end element) and the scan's element count dominate
+  // (profiles/r01_v7: T = 2^20 with L = 7 / 28: 0.87 / 0.64 ms per PRTS)
+  long long Lmin = (T + wave - 1) / wave;
+  if (Lmin > 64) Lmin = 64;
+  return L < Lmin ? Lmin : (L < 1 ? 1 : L);
 }
 
 // Scratch of one fast run (allocated by fast_prepare).
@@ -170,8 +169,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
   }
   switch (phase) {
     case 0:
-      cudaFuncSetAttribute(k_filter_reduce<S, NX, NY>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+      kernel_setup(k_filter_reduce<S, NX, NY>, kStageNT, stage_bytes);
       k_filter_reduce<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
           m, maps, Lc, nch, nfull, sc.agg, npad, L.err);
       L.count("filter_reduce");
@@ -184,15 +182,13 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       break;
     case 1:  // filter finish; for PRTS also folds the smoother chunk elements
       if (a.method == 1) {
-        cudaFuncSetAttribute(k_filter_finish<S, NX, NY, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT, stage_bytes);
         k_filter_finish<S, NX, NY, true><<<gs, kStageNT, stage_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, sc.sagg, npad, sc.egl,
             sc.ecap, L.err);
         L.count("filter_finish_smoother_reduce");
       } else {
-        cudaFuncSetAttribute(k_filter_finish<S, NX, NY, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        kernel_setup(k_filter_finish<S, NX, NY, false>, kStageNT, stage_bytes);
         k_filter_finish<S, NX, NY, false><<<gs, kStageNT, stage_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad,
             a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
@@ -218,8 +214,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       const int st = make_smooth_maps<S, NX>(sc.egl, sc.ecap, Lc, nfull, mean, cov, sm_maps);
       if (st) return st;
       const int smem = kSmoothNT / 32 * SmoothTma<S, NX>::warp + 1024;
-      cudaFuncSetAttribute(k_smoother_finish<S, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem);
+      kernel_setup(k_smoother_finish<S, NX>, kSmoothNT, smem);
       k_smoother_finish<S, NX><<<blocks_for(nch, kSmoothNT), kSmoothNT, smem, L.stream>>>(
           m.t, Lc, nch, nfull, sc.sagg, npad, carry, sm_maps, sc.ecap, mean, cov);
     }
@@ -236,8 +231,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       const int st = make_stage_maps<S, NX, NY>(ms, Lc, ms.t / Lc, smaps);
       if (st) return st;
       if (nch_s > 0) {
-        cudaFuncSetAttribute(k_filter_reduce<S, NX, NY>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+        kernel_setup(k_filter_reduce<S, NX, NY>, kStageNT, stage_bytes);
         k_filter_reduce<S, NX, NY><<<blocks_for(nch_s, kStageNT), kStageNT, stage_bytes,
                                      L.stream>>>(ms, smaps, Lc, nch_s, ms.t / Lc, sc.agg, npad,
                                                  L.err);
@@ -256,8 +250,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       StageMaps smaps;
       const int st = make_stage_maps<S, NX, NY>(ms, Lc, ms.t / Lc, smaps);
       if (st) return st;
-      cudaFuncSetAttribute(k_bwd_finish<S, NX, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           stage_bytes);
+      kernel_setup(k_bwd_finish<S, NX, NY>, kStageNT, stage_bytes);
       k_bwd_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
           ms, smaps, m.t, Lc, nch, ms.t / Lc, sc.agg, npad, sc.egl, sc.ecap, mean, cov, L.err);
       L.count("bwd_finish_tf_combine");

@@ -563,14 +563,9 @@ inline int wide_blocks(long long warps, int per_block) {
 
 template <typename S>
 long long wide_auto_chunk(long long T, int waves) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = kWarps * warp_bytes<S>();
-  cudaFuncSetAttribute(k_wide_finish<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wide_finish<S, true>, 32 * kWarps,
-                                                smem);
-  const long long resident = (long long)(sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1) *
+  const int per_sm = kernel_setup(k_wide_finish<S, true>, 32 * kWarps, smem);
+  const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
                              kWarps * (waves > 0 ? waves : 1);
   const long long L = (T + resident - 1) / resident;
   return L < 1 ? 1 : L;
@@ -586,7 +581,7 @@ void wide_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf, long long n
   bufs.b[1] = ElemBuf<S>{aux1, plan.cap1 ? plan.cap1 : 1, plan.cap1, rev};
   bufs.b[2] = ElemBuf<S>{aux2, plan.cap2 ? plan.cap2 : 1, plan.cap2, rev};
   const int smem = 4 * warp_bytes<S>();
-  cudaFuncSetAttribute(k_level<Ops, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kernel_setup(k_level<Ops, 32>, 128, smem);
   for (const LevelDesc& d : plan.levels) {
     const int g = d.kind == kLvSeqChain ? 1 : (int)std::min<long long>(wide_blocks(d.count, 4),
                                                                        148LL * 16);
@@ -628,7 +623,7 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
   WideFilterOps<S> fops{L.err, nx};
   WideSmootherOps<S> sops{nx};
   // 1. reduce + scan of the filtering chunk elements
-  cudaFuncSetAttribute(k_wide_reduce<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kernel_setup(k_wide_reduce<S>, 32 * kWarps, smem);
   k_wide_reduce<S><<<grid, 32 * kWarps, smem, L.stream>>>(m, Lc, nch, agg, L.err);
   L.count("wide_filter_reduce");
   if (npad > nch) {
@@ -639,15 +634,13 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
   if (npad > 1) wide_scan(L, fops, agg, npad, aux1, aux2, plan, 0);
   // 2. finish
   if (a.method == 0) {
-    cudaFuncSetAttribute(k_wide_finish<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
+    kernel_setup(k_wide_finish<S, false>, 32 * kWarps, smem);
     k_wide_finish<S, false><<<grid, 32 * kWarps, smem, L.stream>>>(
         m, Lc, nch, agg, nullptr, mean, cov, nullptr, nullptr, L.err);
     L.count("wide_filter_finish");
     return 0;
   }
-  cudaFuncSetAttribute(k_wide_finish<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       smem);
+  kernel_setup(k_wide_finish<S, true>, 32 * kWarps, smem);
   k_wide_finish<S, true><<<grid, 32 * kWarps, smem, L.stream>>>(m, Lc, nch, agg, nullptr, mean,
                                                                  cov, sagg, egl, L.err);
   L.count("wide_filter_finish_smoother_reduce");
@@ -658,8 +651,7 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
     L.count("fill_identity");
   }
   if (npad > 1) wide_scan(L, sops, sagg, npad, aux1, aux2, plan, 1);
-  cudaFuncSetAttribute(k_wide_smoother_finish<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       smem);
+  kernel_setup(k_wide_smoother_finish<S>, 32 * kWarps, smem);
   k_wide_smoother_finish<S><<<grid, 32 * kWarps, smem, L.stream>>>(m, Lc, nch, sagg, nullptr,
                                                                    egl, mean, cov);
   L.count("wide_smoother_finish");

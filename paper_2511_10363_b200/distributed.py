@@ -54,6 +54,11 @@ class CudaShardEngine:
         self.nx = self.mk.nx
         import torch
         self.torch = torch
+        # the phases, the element all_gathers (NCCL, torch's current stream)
+        # and the folds are queued back to back on one stream without host
+        # synchronisation; the smoother finish synchronises and reports errors
+        be.set_stream(torch.cuda.current_stream(self.mk.device))
+        be.set_option("shard_async", 1)
         self.dt = torch.float64 if self.mk.f64 else torch.float32
         self.dev = self.mk.device
 
