@@ -53,7 +53,7 @@ inline void check(int st) {
 // one CUDA device.  Host closures cannot run on the device, so run() throws.
 class CudaBackend final : public Backend {
  public:
-  explicit CudaBackend(int device = 0, int mode = PSK_MODE_FAST, int chunk = 64) {
+  explicit CudaBackend(int device = 0, int mode = PSK_MODE_FAST, int chunk = 0) {
     psk_detail::check(psk_create(&ctx_, device));
     psk_detail::check(psk_set_mode(ctx_, mode));
     psk_detail::check(psk_set_chunk(ctx_, chunk));

@@ -1,0 +1,91 @@
+// dropin_check.cpp -- the C++ drop-in exercised end to end (test
+// infrastructure, run by tests/test_gpu_dropin.py on the GPU box).
+//
+// A reference user's program: the UNMODIFIED reference headers
+// (/root/reference/proj/core/include, model generator, drivers, PoolBackend)
+// plus include/parascan_b200/cuda_backend.hpp.  The same call sites run once
+// with the reference's PoolBackend and once with parascan::CudaBackend -- the
+// only change a caller makes -- and the program prints the max relative
+// error (bench.hpp:216-237 metric) of every GPU result against the
+// reference's own result on the same inputs.  Exit 0 iff all are within the
+// FP64 gate (1e-9), and the reference's exception types come back from the
+// GPU path (a non-PD S: NotPositiveDefinite; an empty SenguptaB threshold:
+// ContractViolation).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "parascan/kalman_par.hpp"
+#include "parascan/model_gen.hpp"
+#include "parascan_b200/cuda_backend.hpp"
+
+using namespace parascan;
+
+static double rel_err(const std::vector<GaussianStats<double>>& a,
+                      const std::vector<GaussianStats<double>>& b) {
+  double e = 0;
+  for (std::size_t k = 0; k < a.size(); ++k) {
+    const auto am = a[k].mean.view(), bm = b[k].mean.view();
+    for (int i = 0; i < am.rows; ++i)
+      e = std::fmax(e, std::fabs(am(i, 0) - bm(i, 0)) / (1 + std::fabs(bm(i, 0))));
+    const auto ac = a[k].cov.view(), bc = b[k].cov.view();
+    for (int i = 0; i < ac.rows; ++i)
+      for (int j = 0; j < ac.cols; ++j)
+        e = std::fmax(e, std::fabs(ac(i, j) - bc(i, j)) / (1 + std::fabs(bc(i, j))));
+  }
+  return a.size() == b.size() ? e : 1e300;
+}
+
+int main() {
+  int bad = 0;
+  PoolBackend pool(4);
+  CudaBackend gpu(0), gpu2(0);
+  CudaBackend exact(0, PSK_MODE_EXACT);
+  const int dims[][2] = {{4, 2}, {3, 1}, {8, 4}};
+  for (const auto& d : dims) {
+    const Lgssm<double> m = gen_model(11, d[0], d[1], 1500);
+    const Measurements<double> ys = simulate_data(m, 12);
+    for (ScanAlg alg : {ScanAlg::InplaceLaFi, ScanAlg::Blelloch, ScanAlg::SenguptaB}) {
+      const ScanSpec spec{alg, 16};
+      const double e1 = rel_err(prts_run(m, ys, spec, gpu), prts_run(m, ys, spec, pool));
+      const double e2 = rel_err(pkf_run(m, ys, spec, gpu), pkf_run(m, ys, spec, pool));
+      const double e3 = rel_err(ptfs_run(m, ys, spec, gpu, gpu2, 2),
+                                ptfs_run(m, ys, spec, pool, pool, 2));
+      // exact mode: the reference's own operation order, bitwise
+      const double e4 = rel_err(prts_run(m, ys, spec, exact), prts_run(m, ys, spec, pool));
+      std::printf("nx=%d ny=%d alg=%s prts %.3e pkf %.3e ptfs %.3e exact-prts %.3e\n", d[0],
+                  d[1], to_string(alg), e1, e2, e3, e4);
+      if (!(e1 < 1e-9 && e2 < 1e-9 && e3 < 1e-9 && e4 == 0.0)) ++bad;
+    }
+    const double ed = rel_err(prts_run(m, ys, ScanSpec{kDecoupledLookback, 1}, gpu),
+                              prts_run(m, ys, ScanSpec{ScanAlg::InplaceLaFi, 1}, pool));
+    std::printf("nx=%d ny=%d alg=decoupled_lookback prts %.3e\n", d[0], d[1], ed);
+    if (!(ed < 1e-9)) ++bad;
+  }
+  // error behaviour
+  {
+    Lgssm<double> m = gen_model(3, 4, 2, 50);
+    const Measurements<double> ys = simulate_data(m, 4);
+    bool threw = false;
+    try {
+      prts_run(m, ys, ScanSpec{ScanAlg::SenguptaB, 3}, gpu);
+    } catch (const ContractViolation&) {
+      threw = true;
+    }
+    std::printf("SenguptaB n=3 -> ContractViolation: %s\n", threw ? "yes" : "no");
+    if (!threw) ++bad;
+    m.r[10] = Mat<double>(2, 2);
+    m.r[10].view()(0, 0) = -1e3;
+    m.r[10].view()(1, 1) = -1e3;
+    threw = false;
+    try {
+      pkf_run(m, ys, ScanSpec{ScanAlg::InplaceLaFi, 1}, gpu);
+    } catch (const NotPositiveDefinite&) {
+      threw = true;
+    }
+    std::printf("indefinite S -> NotPositiveDefinite: %s\n", threw ? "yes" : "no");
+    if (!threw) ++bad;
+  }
+  std::printf("%s\n", bad ? "DROPIN FAIL" : "DROPIN OK");
+  return bad ? 1 : 0;
+}
