@@ -380,9 +380,21 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
         float(out.mean[-1, 0])  # the result is on the host
         ts.append(time.perf_counter() - t0)
     sec = sum(ts) / len(ts)
+    # where an end-to-end call goes (CUDA events of one profiled call)
+    be.set_profile(True)
+    psk.prts_run(m, ys, spec, be, out=res)
+    prof = be.last_profile()
+    be.set_profile(False)
+    br = {"h2d_inputs": sum(ms for n, ms in prof if n == "h2d_inputs"),
+          "kernels": sum(ms for n, ms in prof if not n.startswith(("h2d", "d2h"))),
+          "d2h_outputs": sum(ms for n, ms in prof if n == "d2h_outputs")}
     return {"value": T / sec, "unit": "time-steps/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "timer": "wall clock around the synchronous API call"}
+            "timer": "wall clock around the synchronous API call",
+            "breakdown_ms": {k: round(v, 2) for k, v in br.items()},
+            "pcie_note": "pinned copies: H2D ~55.6 GB/s, D2H ~55.0 GB/s on this box "
+                         "(tools/pcie.py); PRTS cannot overlap them (every smoothed output "
+                         "depends on every input)"}
 
 
 if __name__ == "__main__":

@@ -217,6 +217,7 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
   v.ny = ny;
   v.prior_first = 1;
   v.last_step = T - 1;
+  if (host || force_copy) ctx->launch.mark("h2d_inputs");  // profile: copy span
   return PSK_OK;
 }
 
@@ -308,6 +309,7 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     cudaMemcpyAsync(mean, dmean, mb, kind, ctx->stream);
     cudaMemcpyAsync(cov, dcov, cb, kind, ctx->stream);
+    ctx->launch.mark(host ? "d2h_outputs" : "d2d_outputs");
   }
   return PSK_OK;
 }

@@ -68,6 +68,15 @@ struct ExactLaunch {
   }
   // called right after each kernel launch (launches on one stream are
   // serialised, so kernel i spans evs[i] .. evs[i+1])
+  // a profiled span that is not a kernel launch (host <-> device copies)
+  void mark(const char* name) {
+    if (!profile) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    evs.push_back(e);
+    names.push_back(name);
+  }
   void count(const char* name) {
     ++launches;
     if (!profile) return;
