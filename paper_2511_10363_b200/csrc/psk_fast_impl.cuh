@@ -8,6 +8,7 @@
 #include "psk_exact.h"
 #include "psk_fast.cuh"
 #include "psk_levels.cuh"
+#include "psk_tiles.cuh"
 #include "psk_tma.hpp"
 
 namespace psk {
@@ -45,6 +46,43 @@ ModelView<S> shift_model(const ModelView<S>& m) {
   return v;
 }
 
+// Recursive tile sweep (psk_tiles.cuh) of the view `v` of buffer `a`.
+template <class Ops>
+static void tiled_sweep(ExactLaunch& L, const Ops& ops, const ElemBuf<typename Ops::S>& a,
+                        const ElemBuf<typename Ops::S>& orig, TileView v, bool blelloch,
+                        bool outer) {
+  using S = typename Ops::S;
+  const int smem = (int)(sizeof(S) * Ops::kSize * kTileSlots);
+  const ElemBuf<S> none{nullptr, 1, 0, a.rev};
+  const ElemBuf<S> og = outer ? orig : none;
+  if (v.n <= kTile) {
+    if (blelloch) {
+      kernel_setup(k_tile_all<Ops, true>, kTile, smem);
+      k_tile_all<Ops, true><<<1, kTile, smem, L.stream>>>(ops, a, og, v, og);
+    } else {
+      kernel_setup(k_tile_all<Ops, false>, kTile, smem);
+      k_tile_all<Ops, false><<<1, kTile, smem, L.stream>>>(ops, a, none, v, none);
+    }
+    L.count("chunk_scan_tile_all");
+    return;
+  }
+  const int grid = (int)(v.n / kTile);
+  kernel_setup(k_tile_up<Ops>, kTile, smem);
+  k_tile_up<Ops><<<grid, kTile, smem, L.stream>>>(ops, a, og, v, none, ArenaOut{});
+  L.count("chunk_scan_tile_up");
+  tiled_sweep(L, ops, a, orig, TileView{v.n / kTile, v.stride * kTile,
+                                        v.off + (kTile - 1) * v.stride},
+              blelloch, false);
+  if (blelloch) {
+    kernel_setup(k_tile_down<Ops, true>, kTile, smem);
+    k_tile_down<Ops, true><<<grid, kTile, smem, L.stream>>>(ops, a, og, v, none, 0);
+  } else {
+    kernel_setup(k_tile_down<Ops, false>, kTile, smem);
+    k_tile_down<Ops, false><<<grid, kTile, smem, L.stream>>>(ops, a, none, v, none, 0);
+  }
+  L.count("chunk_scan_tile_down");
+}
+
 // Scan of chunk elements: level-by-level plan (alg 0..5) or the single-pass
 // decoupled look-back (alg 6).  `buf` holds npad slots (identity padded).
 template <class Ops>
@@ -61,10 +99,54 @@ static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
   bufs.b[0] = ElemBuf<S>{buf, npad, npad, rev};
   bufs.b[1] = ElemBuf<S>{aux1, plan.cap1 ? plan.cap1 : 1, plan.cap1, rev};
   bufs.b[2] = ElemBuf<S>{aux2, plan.cap2 ? plan.cap2 : 1, plan.cap2, rev};
+  if ((a.alg == 2 || a.alg == 3) && npad >= 2) {
+    // Blelloch / Ladner-Fischer as shared-memory tile sweeps (psk_tiles.cuh)
+    tiled_sweep(L, ops, bufs.b[0], a.alg == 2 ? bufs.b[1] : ElemBuf<S>{nullptr, 1, 0, rev},
+                TileView{npad, 1, 0}, a.alg == 2, true);
+    return;
+  }
+  // Sengupta hybrid: the reduce passes d <= log2(tile) and the distribute
+  // passes d < log2(tile) run as tile sweeps; the rest level by level
+  int sg_levels = 0;  // number of reduce passes (dstar)
+  for (const LevelDesc& d : plan.levels) sg_levels += d.kind == kLvSgReduce;
+  const int tl = (int)log2_exact(kTile);
+  const bool sg_tiled = (a.alg == 4 || a.alg == 5) && sg_levels >= tl;
+  const int smem = (int)(sizeof(S) * Ops::kSize * kTileSlots);
+  const ElemBuf<S> none{nullptr, 1, 0, rev};
+  int reduce_seen = 0;
+  long long root_off = 0;
+  bool dist_tail = false;
   for (const LevelDesc& d : plan.levels) {
+    if (sg_tiled && d.kind == kLvSgReduce) {
+      ++reduce_seen;  // level reduce_seen, arena offset d.p0
+      if (reduce_seen < tl) continue;
+      if (reduce_seen == tl) {
+        ArenaOut ao{};
+        // offsets of arena levels 1..tl (the plan's reduce passes, in order)
+        int q = 0;
+        for (const LevelDesc& e : plan.levels)
+          if (e.kind == kLvSgReduce && q < tl) ao.off[++q] = e.p0;
+        root_off = ao.off[tl];
+        kernel_setup(k_tile_up<Ops>, kTile, smem);
+        k_tile_up<Ops><<<(int)(npad / kTile), kTile, smem, L.stream>>>(
+            ops, bufs.b[0], none, TileView{npad, 1, 0}, bufs.b[1], ao);
+        L.count("chunk_scan_tile_up");
+        continue;
+      }
+    }
+    if (sg_tiled && d.kind == kLvSgDist && d.count > npad / kTile) {
+      dist_tail = true;  // distribute passes below the tile roots: fused
+      continue;
+    }
     const int g = d.kind == kLvSeqChain ? 1 : grid_for(d.count, kBlock);
     k_level<Ops><<<g, kBlock, 0, L.stream>>>(ops, bufs, d);
     L.count("chunk_scan_level");
+  }
+  if (dist_tail) {
+    kernel_setup(k_tile_down<Ops, false>, kTile, smem);
+    k_tile_down<Ops, false><<<(int)(npad / kTile), kTile, smem, L.stream>>>(
+        ops, bufs.b[0], none, TileView{npad, 1, 0}, bufs.b[1], root_off);
+    L.count("chunk_scan_tile_down");
   }
 }
 
