@@ -154,9 +154,12 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     // Device arrays are used in place when the TMA stage (psk_stage.cuh) can
     // read them: 16-byte aligned base, per-step pitch a multiple of 16 bytes,
     // and blocks that are whole 16-byte rows (the stage reads rounded rows).
-    const bool dense_ok = !host && bb % 16 == 0 &&
-                          (reinterpret_cast<uintptr_t>(f[i].src) % 16) == 0 &&
-                          ((size_t)st * sizeof(S)) % 16 == 0;
+    // Dense blocks of 4 / 8 bytes (d, y at small ny in FP32, ...) are used as
+    // they are too: the stage groups 16 / bytes consecutive steps per row.
+    const bool small_dense = bb < 16 && 16 % bb == 0 && (size_t)st * sizeof(S) == bb;
+    const bool dense_ok = !host && (reinterpret_cast<uintptr_t>(f[i].src) % 16) == 0 &&
+                          ((bb % 16 == 0 && ((size_t)st * sizeof(S)) % 16 == 0) ||
+                           small_dense || st == 0);
     if (dense_ok) {
       outp[i] = static_cast<const S*>(f[i].src);
       outs[i] = st;
@@ -166,7 +169,9 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     // transition of a sharded run for f/u/q) at a 16-byte-rounded pitch
     const long long nblk =
         st == 0 ? 1 : (T > 0 ? T : 1) + ((i == 0 || i == 1 || i == 2) ? extra_fuq : 0);
-    const size_t pb = (bb + 15) / 16 * 16;
+    // small dense blocks keep their dense pitch (grouped rows), the rest is
+    // rounded up to whole 16-byte rows
+    const size_t pb = (bb < 16 && 16 % bb == 0) ? bb : (bb + 15) / 16 * 16;
     S* dst = static_cast<S*>(ctx_alloc(pb * (size_t)nblk, ctx));
     if (!dst) return fail(PSK_E_ALLOC, "device allocation failed (model)");
     const cudaMemcpyKind kind = cudaMemcpyDefault;

@@ -493,28 +493,38 @@ struct FilterStage {
   bool direct;
   const ModelView<S>* m;
   long long k;
+  unsigned unstaged;  // bit f: field f is read from global memory
+  unsigned g2, g4;    // bit f: field f packs 2 / 4 steps per staged row
+  int j;              // walk position (k - chunk start)
+  __device__ __forceinline__ bool glob(int f) const { return direct || ((unstaged >> f) & 1u); }
+  // byte offset of step k's block in a grouped row of field f (block bytes
+  // b; chunk starts are row-aligned): branch-free
+  __device__ __forceinline__ int sub(int f, int b) const {
+    const int mask = (int)((g2 >> f) & 1u) | (int)(((g4 >> f) & 1u) * 3u);
+    return (j & mask) * b;
+  }
   __device__ __forceinline__ Mat<S, NX, NX> F() const {
-    return direct || m->sf == 0 ? load<S, NX, NX>(m->F(k))
-                                : tma_get<typename In::F, S, NX, NX>(st, t);
+    return glob(0) ? load<S, NX, NX>(m->F(k))
+                   : tma_get<typename In::F, S, NX, NX>(st, t, sub(0, In::F::bytes));
   }
   __device__ __forceinline__ Vec<S, NX> u() const {
-    return direct || m->su == 0 ? load<S, NX, 1>(m->U(k))
-                                : tma_get<typename In::u, S, NX, 1>(st, t);
+    return glob(1) ? load<S, NX, 1>(m->U(k))
+                   : tma_get<typename In::u, S, NX, 1>(st, t, sub(1, In::u::bytes));
   }
   __device__ __forceinline__ Mat<S, NX, NX> Q() const {
-    return direct || m->sq == 0 ? load<S, NX, NX>(m->Q(k))
-                                : tma_get<typename In::Q, S, NX, NX>(st, t);
+    return glob(2) ? load<S, NX, NX>(m->Q(k))
+                   : tma_get<typename In::Q, S, NX, NX>(st, t, sub(2, In::Q::bytes));
   }
   __device__ __forceinline__ Meas<S, NX, NY> meas() const {
     Meas<S, NX, NY> z;
-    z.H = direct || m->sh == 0 ? load<S, NY, NX>(m->H(k))
-                               : tma_get<typename In::H, S, NY, NX>(st, t);
-    z.d = direct || m->sd == 0 ? load<S, NY, 1>(m->D(k))
-                               : tma_get<typename In::d, S, NY, 1>(st, t);
-    z.R = direct || m->sr == 0 ? load<S, NY, NY>(m->R(k))
-                               : tma_get<typename In::R, S, NY, NY>(st, t);
-    z.y = direct || m->sy == 0 ? load<S, NY, 1>(m->Y(k))
-                               : tma_get<typename In::y, S, NY, 1>(st, t);
+    z.H = glob(3) ? load<S, NY, NX>(m->H(k))
+                  : tma_get<typename In::H, S, NY, NX>(st, t, sub(3, In::H::bytes));
+    z.d = glob(4) ? load<S, NY, 1>(m->D(k))
+                  : tma_get<typename In::d, S, NY, 1>(st, t, sub(4, In::d::bytes));
+    z.R = glob(5) ? load<S, NY, NY>(m->R(k))
+                  : tma_get<typename In::R, S, NY, NY>(st, t, sub(5, In::R::bytes));
+    z.y = glob(6) ? load<S, NY, 1>(m->Y(k))
+                  : tma_get<typename In::y, S, NY, 1>(st, t, sub(6, In::y::bytes));
     return z;
   }
 };
@@ -538,14 +548,21 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
   const bool tma = cta0 < nfull;                            // CTA-uniform
   const long long jn = min(L, m.t - cta0 * L);
   const bool direct = !tma || cta0 + t >= nfull;
+  unsigned unstaged = 0, g2 = 0, g4 = 0;  // per-field flags, in registers
+#pragma unroll
+  for (int f = 0; f < 7; ++f) {
+    unstaged |= (maps.use[f] ? 0u : 1u) << f;
+    g2 |= (maps.grp[f] == 2 ? 1u : 0u) << f;
+    g4 |= (maps.grp[f] == 4 ? 1u : 0u) << f;
+  }
   auto issue = [&](int s, long long j) {
     fence_proxy_async();  // generic reads of this stage (last use) before the refill
     mbar_expect_tx(&bars[s], maps.tx);
 #pragma unroll
     for (int f = 0; f < 7; ++f)
       if (maps.use[f])
-        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j, (int)cta0,
-                    &bars[s]);
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)(j / maps.grp[f]),
+                    (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {
     mbar_init(&bars[0], 1);
@@ -558,7 +575,7 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
     const int s = (int)(j & 1);
     if (tma && t == 0 && j + 1 < jn) issue(s ^ 1, j + 1);
     if (tma) mbar_wait(&bars[s], (unsigned)((j >> 1) & 1));
-    if (k0 + j < k1) body(k0 + j, St{sm + s * In::stage, t, direct, &m, k0 + j});
+    if (k0 + j < k1) body(k0 + j, St{sm + s * In::stage, t, direct, &m, k0 + j, unstaged, g2, g4, (int)j});
     __syncthreads();  // stage s is refilled by the next iteration's issue
   }
 }
@@ -581,6 +598,13 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
   const long long cta0 = (long long)blockIdx.x * kStageNT;
   const bool tma = cta0 < nfull;
   const bool direct = !tma || cta0 + t >= nfull;
+  unsigned unstaged = 0, g2 = 0, g4 = 0;  // per-field flags, in registers
+#pragma unroll
+  for (int f = 0; f < 7; ++f) {
+    unstaged |= (maps.use[f] ? 0u : 1u) << f;
+    g2 |= (maps.grp[f] == 2 ? 1u : 0u) << f;
+    g4 |= (maps.grp[f] == 4 ? 1u : 0u) << f;
+  }
   // positions >= the m-length of the CTA's first chunk carry no data
   const long long jd = min(jn, max(0LL, m.t - cta0 * L));
   auto issue = [&](int s, long long j) {
@@ -589,7 +613,8 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
 #pragma unroll
     for (int f = 0; f < 7; ++f)
       if (maps.use[f])
-        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j, (int)cta0, &bars[s]);
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)(j / maps.grp[f]),
+                    (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {
     mbar_init(&bars[0], 1);
@@ -607,7 +632,7 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
       if (tma) mbar_wait(&bars[s], (unsigned)((it >> 1) & 1));
     }
     const long long k = k0 + j;
-    if (k < k1) body(k, k < m.t, St{sm + s * In::stage, t, direct, &m, k});
+    if (k < k1) body(k, k < m.t, St{sm + s * In::stage, t, direct, &m, k, unstaged, g2, g4, (int)j});
     __syncthreads();
     if (data) ++it;
   }

@@ -157,8 +157,22 @@ static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
 // kernels closer to the HBM roof; 4 is the measured optimum at T = 2^24
 // (profiles/r01_v3: L = 64/74/111/148/222/443 -> 5.08/4.96/4.85/4.99/5.03/
 // 5.17 ms per PRTS) ...
+// Steps per staged row of the model's smallest dense field (StageMaps::grp):
+// chunk starts must fall on row boundaries.
 template <typename S, int NX, int NY>
-long long auto_chunk(long long T, int waves) {
+int group_mult(const ModelView<S>& m) {
+  const long long st[7] = {m.sf, m.su, m.sq, m.sh, m.sd, m.sr, m.sy};
+  const int blk[7] = {NX * NX, NX, NX * NX, NY * NX, NY, NY * NY, NY};
+  int g = 1;
+  for (int f = 0; f < 7; ++f) {
+    const int b = blk[f] * (int)sizeof(S);
+    if (b < 16 && 16 % b == 0 && st[f] == blk[f] && 16 / b > g) g = 16 / b;
+  }
+  return g;
+}
+
+template <typename S, int NX, int NY>
+long long auto_chunk(long long T, int waves, int mult = 1) {
   const int per_sm = kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT,
                                   FilterTma<S, NX, NY>::smem);
   const long long wave = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kStageNT;
@@ -169,7 +183,12 @@ long long auto_chunk(long long T, int waves) {
   // (profiles/r01_v7: T = 2^20 with L = 7 / 28: 0.87 / 0.64 ms per PRTS)
   long long Lmin = (T + wave - 1) / wave;
   if (Lmin > 64) Lmin = 64;
-  return L < Lmin ? Lmin : (L < 1 ? 1 : L);
+  long long r = L < Lmin ? Lmin : (L < 1 ? 1 : L);
+  // a multiple of the row grouping of the small dense fields (chunk starts
+  // on row boundaries).  (L within +-15 % of this choice measures within run
+  // noise, 4.74-4.90 ms at 2^24: profiles/r01_v9/chunk_landscape.txt.)
+  if (r > mult) r = (r + mult - 1) / mult * mult;
+  return r;
 }
 
 // Scratch of one fast run (allocated by fast_prepare).
@@ -189,7 +208,7 @@ template <typename S, int NX, int NY>
 static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<S>& sc,
                           void* (*alloc)(size_t, void*), void* actx) {
   const long long T = m.t;
-  sc.chunk = a.chunk >= 1 ? a.chunk : auto_chunk<S, NX, NY>(T, a.waves);
+  sc.chunk = a.chunk >= 1 ? a.chunk : auto_chunk<S, NX, NY>(T, a.waves, group_mult<S, NX, NY>(m));
   sc.nchunks = T > 0 ? (T + sc.chunk - 1) / sc.chunk : 0;
   const bool dlb = a.alg == 6;
   sc.npad = (dlb || a.alg == 0) ? sc.nchunks : (long long)next_pow2(sc.nchunks);
@@ -375,7 +394,8 @@ static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, Exact
                         void* (*allocB)(size_t, void*), void* ctxB) {
   if (mA.t == 0) return 0;
   a.method = 2;
-  if (a.chunk < 1) a.chunk = auto_chunk<S, NX, NY>(mA.t, a.waves);  // same L on both sides
+  if (a.chunk < 1)  // same L on both sides
+    a.chunk = auto_chunk<S, NX, NY>(mA.t, a.waves, group_mult<S, NX, NY>(mA));
   FastScratch<S> sa, sb;
   cudaSetDevice(devB);
   int st = fast_prepare_t<S, NX, NY>(mB, a, sb, allocB, ctxB);

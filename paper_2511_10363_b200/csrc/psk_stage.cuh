@@ -109,8 +109,10 @@ __device__ __forceinline__ int tma_off(int r, int c) {
   return a ^ (((a >> 7) & ((1 << F::swz) - 1)) << 4);
 }
 // this thread's block of a staged field as a row-major R x C matrix
+// `sub`: byte offset of this step's block inside a row that packs several
+// steps of a small field (grouped rows, see StageMaps::grp); 0 otherwise.
 template <class F, typename S, int R, int C>
-__device__ __forceinline__ Mat<S, R, C> tma_get(const unsigned char* stage, int t) {
+__device__ __forceinline__ Mat<S, R, C> tma_get(const unsigned char* stage, int t, int sub = 0) {
   static_assert(R * C * (int)sizeof(S) == F::bytes, "field size");
   Mat<S, R, C> m;
   S* o = &m.a[0][0];
@@ -118,7 +120,7 @@ __device__ __forceinline__ Mat<S, R, C> tma_get(const unsigned char* stage, int 
   constexpr int n = R * C;
 #pragma unroll
   for (int c = 0; c < (n + per - 1) / per; ++c) {
-    const unsigned char* p = stage + F::off + tma_off<F>(t, c);
+    const unsigned char* p = stage + F::off + tma_off<F>(t, c) + sub;
     if ((c + 1) * per <= n) {
       const float4 v = *reinterpret_cast<const float4*>(p);
       const S* vs = reinterpret_cast<const S*>(&v);
@@ -180,6 +182,11 @@ __device__ __forceinline__ void tma_put(unsigned char* stage, int t, const Mat<S
 struct StageMaps {
   CUtensorMap m[7];
   int use[7];
+  // steps per 16-byte row: a field whose per-step block is 4 or 8 bytes and
+  // dense (e.g. d, y at ny = 2 in FP32) is viewed as rows of 16 / bytes
+  // consecutive steps, so it is staged in place instead of re-pitched; the
+  // box of walk position j is row j / grp, the step's block at (j % grp)
+  int grp[7];
   unsigned tx;  // bytes one stage receives (sum of the used boxes)
 };
 

@@ -28,9 +28,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 }
 
 // Fill `maps` for a staged walk over chunks of L steps, `nfull` of them
-// complete.  Returns 0, or 9 when a non-broadcast field cannot be described
-// (prepare_model packs every field into a TMA-compatible pitch, so this
-// signals a bug rather than a user error).
+// complete.  A field is staged when its per-step blocks are whole 16-byte
+// rows, or dense blocks of 4 / 8 bytes grouped 16 / bytes steps per row (L a
+// multiple of that); any other non-broadcast field (a grouped field viewed
+// at an odd step offset, as the PTFS backward pass's shifted model is) is
+// read from global memory by the kernels.  Returns 0, or 9 when the TMA
+// encoder is unavailable or rejects a map.
 // L2 promotion of the staged boxes (experiment knobs for the ncu traffic
 // check, 0..3 = none / 64 / 128 / 256 bytes): PSK_TMA_L2PROMO for rows of 64
 // bytes and more (default 256), PSK_TMA_L2PROMO_SMALL for smaller rows
@@ -61,14 +64,31 @@ int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMa
   maps.tx = 0;
   for (int f = 0; f < 7; ++f) {
     maps.use[f] = 0;
+    maps.grp[f] = 1;
     if (stride[f] == 0 || nfull <= 0) continue;  // broadcast: read from global
     auto enc = tma_encoder();
+    if (!enc) return 9;
     const int row = In::row(f);
+    const int bytes = (f == 0 || f == 2) ? NX * NX * (int)sizeof(S)
+                      : f == 1           ? NX * (int)sizeof(S)
+                      : f == 3           ? NY * NX * (int)sizeof(S)
+                      : f == 5           ? NY * NY * (int)sizeof(S)
+                                         : NY * (int)sizeof(S);
     const unsigned long long pitch = (unsigned long long)stride[f] * sizeof(S);
-    if (!enc || reinterpret_cast<uintptr_t>(base[f]) % 16 || pitch % 16 || pitch < (unsigned)row)
-      return 9;
-    cuuint64_t dims[3] = {(cuuint64_t)(row / sizeof(S)), (cuuint64_t)L, (cuuint64_t)nfull};
-    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * (cuuint64_t)L};
+    const bool aligned = reinterpret_cast<uintptr_t>(base[f]) % 16 == 0;
+    long long g = 1;  // steps per row
+    if (aligned && pitch % 16 == 0 && pitch >= (unsigned long long)row) {
+      g = 1;
+    } else if (aligned && bytes < 16 && 16 % bytes == 0 && pitch == (unsigned long long)bytes &&
+               L % (16 / bytes) == 0) {
+      g = 16 / bytes;  // dense small blocks: rows of g consecutive steps
+    } else {
+      continue;  // not stageable (a grouped field at an odd step offset): global loads
+    }
+    const unsigned long long rpitch = g == 1 ? pitch : 16;  // bytes between rows
+    cuuint64_t dims[3] = {(cuuint64_t)(row / sizeof(S)), (cuuint64_t)(L / g),
+                          (cuuint64_t)nfull};
+    cuuint64_t strides[2] = {(cuuint64_t)rpitch, (cuuint64_t)(pitch * (unsigned long long)L)};
     cuuint32_t box[3] = {(cuuint32_t)(row / sizeof(S)), 1, (cuuint32_t)kStageNT};
     cuuint32_t es[3] = {1, 1, 1};
     const CUtensorMapSwizzle sw = row == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -82,6 +102,7 @@ int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMa
             stage_l2_promotion(row), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 9;
     maps.use[f] = 1;
+    maps.grp[f] = (int)g;
     maps.tx += (unsigned)(row * kStageNT);
   }
   return 0;
