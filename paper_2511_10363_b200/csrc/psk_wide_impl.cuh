@@ -42,10 +42,29 @@ constexpr int warp_bytes() {
   return (kMatSlots * kMat + kVecSlots * kVec) * (int)sizeof(S);
 }
 template <typename S>
-__device__ __forceinline__ Slots<S> warp_slots() {
+__device__ __forceinline__ Slots<S> warp_slots(int nm = kMatSlots) {
   extern __shared__ __align__(16) unsigned char wsm[];
-  S* base = reinterpret_cast<S*>(wsm) + (threadIdx.x >> 5) * (warp_bytes<S>() / (int)sizeof(S));
-  return Slots<S>{base, kMatSlots};
+  S* base = reinterpret_cast<S*>(wsm) + (threadIdx.x >> 5) * (nm * kMat + kVecSlots * kVec);
+  return Slots<S>{base, nm};
+}
+// Matrix slots of the per-step kernels: A, C, J, 7 scratch, plus one per
+// model matrix (F, Q, H, R) that varies with the step -- a time-invariant
+// (stride-0) matrix is read in place from global memory (L1-resident), which
+// frees its slot: BASELINE configs[4]'s broadcast models run 10 slots/warp.
+// (FP64 only: FP32 slots are half the size and occupancy is set by
+// registers, so FP32 keeps every matrix in shared memory.)
+template <typename S>
+__host__ __device__ __forceinline__ bool staged_input(long long stride) {
+  return stride != 0 || sizeof(S) == 4;
+}
+template <typename S>
+__host__ __device__ __forceinline__ int step_slots(const ModelView<S>& m) {
+  return 10 + staged_input<S>(m.sf) + staged_input<S>(m.sq) + staged_input<S>(m.sh) +
+         staged_input<S>(m.sr);
+}
+template <typename S>
+__host__ __device__ __forceinline__ int step_smem(int nm) {
+  return kWarps * (nm * kMat + kVecSlots * kVec) * (int)sizeof(S);
 }
 
 template <typename S>
@@ -218,29 +237,47 @@ template <typename S>
 struct Step {
   Slots<S> sc;
   int nx, ny;
+  const S *fg, *qg, *hg, *rg;  // broadcast model matrices in global memory
+  int fs, qs, hs, rs;          // their slots when staged per step (-1: global)
+  __device__ Step(const ModelView<S>& m, int nx_, int ny_)
+      : sc(warp_slots<S>(step_slots(m))), nx(nx_), ny(ny_), fg(m.f), qg(m.q), hg(m.h),
+        rg(m.r) {
+    int k = 10;
+    fs = staged_input<S>(m.sf) ? k++ : -1;
+    qs = staged_input<S>(m.sq) ? k++ : -1;
+    hs = staged_input<S>(m.sh) ? k++ : -1;
+    rs = staged_input<S>(m.sr) ? k++ : -1;
+  }
   __device__ WM<S> A() const { return mat(sc.m(0)); }
   __device__ WM<S> C() const { return mat(sc.m(1)); }
   __device__ WM<S> J() const { return mat(sc.m(2)); }
-  __device__ WM<S> F() const { return mat(sc.m(3)); }
-  __device__ WM<S> Q() const { return mat(sc.m(4)); }
-  __device__ WM<S> H() const { return mat(sc.m(5)); }
-  __device__ WM<S> R() const { return mat(sc.m(6)); }
-  __device__ WM<S> T(int i) const { return mat(sc.m(7 + i)); }  // i < 7
+  __device__ WM<S> F() const { return fs >= 0 ? mat(sc.m(fs)) : WM<S>{const_cast<S*>(fg), nx}; }
+  __device__ WM<S> Q() const { return qs >= 0 ? mat(sc.m(qs)) : WM<S>{const_cast<S*>(qg), nx}; }
+  __device__ WM<S> H() const { return hs >= 0 ? mat(sc.m(hs)) : WM<S>{const_cast<S*>(hg), nx}; }
+  __device__ WM<S> R() const { return rs >= 0 ? mat(sc.m(rs)) : WM<S>{const_cast<S*>(rg), ny}; }
+  __device__ WM<S> T(int i) const { return mat(sc.m(3 + i)); }  // i < 7
   __device__ WM<S> b() const { return vec(sc.v(0)); }
   __device__ WM<S> eta() const { return vec(sc.v(1)); }
   __device__ WM<S> u() const { return vec(sc.v(2)); }
   __device__ WM<S> d() const { return vec(sc.v(3)); }
   __device__ WM<S> y() const { return vec(sc.v(4)); }
   __device__ WM<S> t(int i) const { return vec(sc.v(5 + i)); }  // i < 9
-  // model blocks of step k (coalesced)
+  // model blocks of step k (coalesced); broadcast matrices stay in place
   __device__ void load(const ModelView<S>& m, long long k) const {
-    gload(F(), m.F(k), nx, nx);
-    gload(Q(), m.Q(k), nx, nx);
+    if (fs >= 0) gload(F(), m.F(k), nx, nx);
+    if (qs >= 0) gload(Q(), m.Q(k), nx, nx);
+    if (hs >= 0) gload(H(), m.H(k), ny, nx);
+    if (rs >= 0) gload(R(), m.R(k), ny, ny);
     gload(u(), m.U(k), nx, 1);
-    gload(H(), m.H(k), ny, nx);
     gload(d(), m.D(k), ny, 1);
-    gload(R(), m.R(k), ny, ny);
     gload(y(), m.Y(k), ny, 1);
+    __syncwarp();
+  }
+  // the transition of step k into the F / Q / u slots (chunk-end element)
+  __device__ void load_fqu(const ModelView<S>& m, long long k) const {
+    if (fs >= 0) gload(F(), m.F(k), nx, nx);
+    if (qs >= 0) gload(Q(), m.Q(k), nx, nx);
+    gload(u(), m.U(k), nx, 1);
     __syncwarp();
   }
 };
@@ -260,7 +297,7 @@ __device__ void cond_update(const Step<S>& st, unsigned& err) {
   gemm<false, false>(ha, st.H(), st.A(), ny, nx, nx);
   gemm<false, false>(v, st.H(), st.b(), ny, nx, 1, st.y().p, 1, S(-1));
   vadd(v, v, st.d(), ny, S(-1));
-  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, kLd, S(1), true);
+  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, st.R().ld, S(1), true);
   copy(kt, hc, ny, nx);
   copy(wm, ha, ny, nx);
   copy(sv, v, ny, 1);
@@ -280,7 +317,7 @@ __global__ void __launch_bounds__(32 * kWarps)
   const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= nchunks) return;  // warp-uniform
   const int nx = m.nx, ny = m.ny;
-  const Step<S> st{warp_slots<S>(), nx, ny};
+  const Step<S> st(m, nx, ny);
   unsigned e = 0;
   const long long k0 = c * L, k1 = min(k0 + L, m.t);
   // identity, or the prior in state form for the chunk holding step 1
@@ -305,7 +342,7 @@ __global__ void __launch_bounds__(32 * kWarps)
     gemm<false, false>(st.t(2), st.F(), st.b(), nx, nx, 1, st.u().p, 1);
     copy(st.b(), st.t(2), nx, 1);
     gemm<false, false>(st.T(6), st.F(), st.C(), nx, nx, nx);
-    gemm<false, true>(st.C(), st.T(6), st.F(), nx, nx, nx, st.Q().p, kLd, S(1), true);
+    gemm<false, true>(st.C(), st.T(6), st.F(), nx, nx, nx, st.Q().p, st.Q().ld, S(1), true);
     cond_update(st, e);
   }
   const FOffs F(nx);
@@ -380,7 +417,7 @@ __device__ void kf_update(const Step<S>& st, unsigned& err) {
   gemm<false, false>(hc, st.H(), st.C(), ny, nx, nx);
   gemm<false, false>(v, st.H(), st.b(), ny, nx, 1, st.y().p, 1, S(-1));
   vadd(v, v, st.d(), ny, S(-1));
-  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, kLd, S(1), true);
+  gemm<false, true>(aug, hc, st.H(), ny, nx, ny, st.R().p, st.R().ld, S(1), true);
   copy(kt, hc, ny, nx);
   copy(sv, v, ny, 1);
   gauss_jordan(aug, ny, w, false, err);
@@ -392,7 +429,7 @@ template <typename S>
 __device__ void predict(const Step<S>& st) {
   const int n = st.nx;
   gemm<false, false>(st.T(0), st.F(), st.C(), n, n, n);
-  gemm<false, true>(st.T(1), st.T(0), st.F(), n, n, n, st.Q().p, kLd, S(1), true);
+  gemm<false, true>(st.T(1), st.T(0), st.F(), n, n, n, st.Q().p, st.Q().ld, S(1), true);
   gemm<false, false>(st.t(2), st.F(), st.b(), n, n, 1, st.u().p, 1);
 }
 
@@ -406,7 +443,7 @@ __global__ void __launch_bounds__(32 * kWarps)
   const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= nchunks) return;
   const int nx = m.nx, ny = m.ny;
-  const Step<S> st{warp_slots<S>(), nx, ny};
+  const Step<S> st(m, nx, ny);
   unsigned e = 0;
   const long long k0 = c * L, k1 = min(k0 + L, m.t);
   const FOffs FO(nx);
@@ -471,10 +508,7 @@ __global__ void __launch_bounds__(32 * kWarps)
     if (k1 - 1 == m.last_step) {
       terminal_elem(st);
     } else {
-      gload(st.F(), m.F(k1), nx, nx);
-      gload(st.Q(), m.Q(k1), nx, nx);
-      gload(st.u(), m.U(k1), nx, 1);
-      __syncwarp();
+      st.load_fqu(m, k1);
       predict(st);
       smoother_elem_pred(st, e);
     }
@@ -497,7 +531,7 @@ __global__ void __launch_bounds__(32 * kWarps)
   const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= nchunks) return;
   const int n = m.nx;
-  const Step<S> st{warp_slots<S>(), n, m.ny};
+  const Step<S> st(m, n, m.ny);
   const long long k0 = c * L, k1 = min(k0 + L, m.t);
   const SOffs SO(n);
   WM<S> gs = st.t(0), Ls = st.C();
@@ -562,8 +596,8 @@ inline int wide_blocks(long long warps, int per_block) {
 }
 
 template <typename S>
-long long wide_auto_chunk(long long T, int waves) {
-  const int smem = kWarps * warp_bytes<S>();
+long long wide_auto_chunk(long long T, int waves, int nm) {
+  const int smem = step_smem<S>(nm);
   const int per_sm = kernel_setup(k_wide_finish<S, true>, 32 * kWarps, smem);
   const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
                              kWarps * (waves > 0 ? waves : 1);
@@ -600,7 +634,8 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
   const long long T = m.t;
   if (T == 0) return 0;
   const int nx = m.nx;
-  const long long Lc = a.chunk >= 1 ? a.chunk : wide_auto_chunk<S>(T, a.waves);
+  const int nm = step_slots(m);
+  const long long Lc = a.chunk >= 1 ? a.chunk : wide_auto_chunk<S>(T, a.waves, nm);
   const long long nch = (T + Lc - 1) / Lc;
   const int alg = a.alg == 6 ? 3 : a.alg;
   const long long npad = alg == 0 ? nch : (long long)next_pow2(nch);
@@ -618,7 +653,7 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
   S* sagg = a.method == 1 ? (S*)alloc(sizeof(S) * SS * npad, actx) : nullptr;
   S* egl = a.method == 1 ? (S*)alloc(sizeof(S) * SS * T, actx) : nullptr;
   if (!agg || !aux1 || !aux2 || (a.method == 1 && (!sagg || !egl))) return 8;
-  const int smem = kWarps * warp_bytes<S>();
+  const int smem = step_smem<S>(nm);
   const int grid = wide_blocks(nch, kWarps);
   WideFilterOps<S> fops{L.err, nx};
   WideSmootherOps<S> sops{nx};
