@@ -264,8 +264,13 @@ def run_psk(args) -> None:
     stream = torch.cuda.Stream(device=dev)
     be = psk.CudaBackend(local, mode="fast", chunk=args.chunk, stream=stream)
 
-    def step(profile: bool = False):
-        be.set_profile(profile)
+    # Device-resident steps are queued back to back ("async": each call returns
+    # once its kernels are on the stream; errors and the per-kernel CUDA-event
+    # spans are collected by be.sync() after the timed region), so the timed
+    # region is GPU time, not host round trips between synchronous calls.
+    be.set_option("async", 1)
+
+    def step():
         with torch.cuda.stream(stream):
             out = dist_psk.prts_run_sharded(model, ys, spec, be, rank, world, lo, hi, T, pg)
         return out
@@ -273,22 +278,26 @@ def run_psk(args) -> None:
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    be.sync()
     if pg is not None:
         torch.distributed.barrier()
     launches = 0
     prof: dict[str, list[float]] = {}
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    be.set_profile(True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            step(profile=True)
+            step()
             launches += be.last_launch_count()
-            for name, ms in be.last_profile():
-                prof.setdefault(name, []).append(ms)
         ev1.record(stream)
         torch.cuda.synchronize()
+    be.sync()  # raises on any device error of the timed steps
+    be.set_profile(False)
+    for name, kms in be.last_profile():
+        prof.setdefault(name, []).append(kms)
     ms = ev0.elapsed_time(ev1) / args.steps
     if pg is not None:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)

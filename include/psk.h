@@ -102,11 +102,18 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
  *   "chunk"     steps folded per thread, 0 = auto (same as psk_set_chunk)
  *   "waves"     auto chunk: the chunks fill this many waves of co-resident
  *               threads (default 4)
+ *   "async"     1: psk_pkf / psk_prts / psk_ptfs return once their work is
+ *               queued on the context's stream (outputs valid when the stream
+ *               completes; errors are reported by psk_sync); default 0 =
+ *               synchronous, like the reference's drivers
  *   "shard_async"  1: the shard phases before psk_shard_smoother_finish and
  *               the folds return without synchronising the stream (errors
  *               are reported by the smoother finish); default 0
  * Returns PSK_E_ARG for an unknown key or value. */
 int psk_set_option(psk_ctx* ctx, const char* key, int64_t value);
+/* Wait for the context's queued work and report the first device error since
+ * the last synchronising call (async mode). */
+int psk_sync(psk_ctx* ctx);
 /* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).
  * The entry points are synchronous: outputs are valid on return. */
 int psk_set_stream(psk_ctx* ctx, void* stream);

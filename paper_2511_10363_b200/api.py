@@ -170,6 +170,11 @@ class CudaBackend:
         if stream is not None:
             self.set_stream(stream)
 
+    def sync(self) -> None:
+        """Wait for queued work; raise the first device error since the last
+        synchronising call (async mode, option "async")."""
+        _check(_lib.lib().psk_sync(self._ctx))
+
     def set_option(self, key: str, value: int) -> None:
         _check(_lib.lib().psk_set_option(self._ctx, key.encode(), int(value)))
 

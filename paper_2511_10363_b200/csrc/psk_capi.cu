@@ -40,6 +40,7 @@ struct psk_ctx {
   long long chunk = 0;  // 0: auto (whole waves of chunks)
   int waves = 4;        // waves of chunks for the auto chunk length
   int shard_async = 0;  // shard phases 0-2 and folds return without a host sync
+  int async = 0;        // drivers return once queued; psk_sync reports errors
   unsigned* d_err = nullptr;
   std::mutex mu;
   ExactLaunch launch;
@@ -336,10 +337,20 @@ int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
   DeviceGuard dg(ctx->device);
   ctx->launch.stream = ctx->stream;
   ctx->launch.err = ctx->d_err;
-  ctx->launch.start();
-  cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  // "async" mode: the call returns once its work is queued on the stream;
+  // the device error word accumulates and the per-kernel event spans are
+  // kept until psk_sync reports them
+  ctx->launch.start(ctx->async != 0);
+  if (!ctx->async) cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   st = m->dtype == PSK_F64 ? run_typed<double>(ctx, m, method, alg, sengupta_n, mean, cov)
                            : run_typed<float>(ctx, m, method, alg, sengupta_n, mean, cov);
+  if (ctx->async) {
+    ctx_free_all(ctx);  // stream-ordered frees
+    if (st) return st;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+    return PSK_OK;
+  }
   unsigned herr = 0;
   cudaMemcpyAsync(&herr, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
   ctx_free_all(ctx);
@@ -451,13 +462,13 @@ int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   DeviceGuard dg(ctx->device);
   ctx->launch.stream = ctx->stream;
   ctx->launch.err = ctx->d_err;
-  ctx->launch.start();
+  ctx->launch.start(ctx->async != 0);
   // "shard_async": the phases before the smoother finish return without a
   // host synchronisation (the error word accumulates and is checked by the
   // final phase), so a rank's phases and its NCCL exchanges stay queued on
-  // the stream back to back
-  const bool defer = ctx->shard_async && phase != 3;
-  if (!ctx->shard_async || phase == 0)
+  // the stream back to back; "async": no phase synchronises (psk_sync does)
+  const bool defer = (ctx->shard_async && phase != 3) || ctx->async;
+  if (!ctx->async && (!ctx->shard_async || phase == 0))
     cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   int st = m->dtype == PSK_F64
                ? shard_typed<double>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out)
@@ -482,15 +493,16 @@ int fold_entry(psk_ctx* ctx, int kind, int dtype, int nx, const void* elems, int
   DeviceGuard dg(ctx->device);
   ctx->launch.stream = ctx->stream;
   ctx->launch.err = ctx->d_err;
-  ctx->launch.start();
-  if (!ctx->shard_async) cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
+  ctx->launch.start(ctx->async != 0);
+  if (!ctx->shard_async && !ctx->async)
+    cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   int st = dtype == PSK_F64
                ? fast_fold<double>(ctx->launch, kind, nx, static_cast<const double*>(elems),
                                    count, static_cast<double*>(out))
                : fast_fold<float>(ctx->launch, kind, nx, static_cast<const float*>(elems),
                                   count, static_cast<float*>(out));
   if (st) st = fail(PSK_E_ARG, "fold failed");
-  if (ctx->shard_async) {  // see shard_entry
+  if (ctx->shard_async || ctx->async) {  // see shard_entry
     if (st) return st;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
@@ -670,6 +682,9 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   if (k == "chunk") {
     if (value < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
     c->chunk = value;
+  } else if (k == "async") {
+    if (value != 0 && value != 1) return fail(PSK_E_ARG, "async must be 0 or 1");
+    c->async = (int)value;
   } else if (k == "shard_async") {
     if (value != 0 && value != 1) return fail(PSK_E_ARG, "shard_async must be 0 or 1");
     c->shard_async = (int)value;
@@ -679,6 +694,35 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   } else {
     return fail(PSK_E_ARG, "unknown option " + k);
   }
+  return PSK_OK;
+}
+
+int psk_sync(psk_ctx* c) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard dg(c->device);
+  unsigned herr = 0;
+  cudaMemcpyAsync(&herr, c->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream);
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaMemsetAsync(c->d_err, 0, sizeof(unsigned), c->stream);
+  // per-kernel spans of every call since the last synchronisation
+  c->profile.clear();
+  auto drain = [&](std::vector<cudaEvent_t>& evs, std::vector<const char*>& names) {
+    for (size_t i = 0; i + 1 < evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
+      c->profile.emplace_back(names[i], ms);
+    }
+    for (auto ev : evs) cudaEventDestroy(ev);
+    evs.clear();
+    names.clear();
+  };
+  for (auto& p : c->launch.pending) drain(p.first, p.second);
+  c->launch.pending.clear();
+  drain(c->launch.evs, c->launch.names);
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  if (herr & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
   return PSK_OK;
 }
 

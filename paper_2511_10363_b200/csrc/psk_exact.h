@@ -55,9 +55,15 @@ struct ExactLaunch {
   bool profile = false;
   std::vector<const char*> names;
   std::vector<cudaEvent_t> evs;  // evs[0] = start; kernel i ends at evs[i+1]
-  void start() {
+  // async mode: the event spans of calls not yet synchronised
+  std::vector<std::pair<std::vector<cudaEvent_t>, std::vector<const char*>>> pending;
+  void start(bool keep = false) {
     launches = 0;
-    for (auto e : evs) cudaEventDestroy(e);
+    if (keep && !evs.empty()) {
+      pending.emplace_back(std::move(evs), std::move(names));
+    } else {
+      for (auto e : evs) cudaEventDestroy(e);
+    }
     evs.clear();
     names.clear();
     if (!profile) return;

@@ -168,6 +168,37 @@ def test_ptfs_two_contexts(psk, gpu, port, dtype):
         assert np.array_equal(_np(dev.mean), psk.ptfs_run(m, ys, spec6, fwd, bwd, 2).mean)
 
 
+def test_async_mode(psk, gpu, port):
+    """option "async": calls return once queued; results are those of the
+    synchronous calls, errors surface at psk_sync (reference exception types)."""
+    import torch
+    m, ys = gen(port, 61, 4, 2, 4000)
+    t = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    md = psk.Lgssm(f=t(m.f), u=t(m.u), q=t(m.q), h=t(m.h), d=t(m.d), r=t(m.r),
+                   prior_mean=t(m.prior_mean), prior_cov=t(m.prior_cov), t=m.t)
+    spec = psk.ScanSpec(psk.ScanAlg(6))
+    ref = psk.CudaBackend(gpu)
+    want = psk.prts_run(md, t(ys), spec, ref)
+    be = psk.CudaBackend(gpu)
+    be.set_option("async", 1)
+    be.set_profile(True)
+    outs = [psk.prts_run(md, t(ys), spec, be) for _ in range(3)]
+    be.sync()
+    names = [n for n, _ in be.last_profile()]
+    assert names.count("smoother_finish") == 3  # spans of all queued calls
+    for o in outs:
+        assert torch.equal(o.mean, want.mean) and torch.equal(o.cov, want.cov)
+    bad = psk.Lgssm(f=md.f, u=md.u, q=md.q, h=md.h, d=md.d, r=md.r.clone(),
+                    prior_mean=md.prior_mean, prior_cov=md.prior_cov, t=m.t)
+    bad.r[10] = -1e3 * torch.eye(2, device="cuda", dtype=bad.r.dtype)
+    psk.pkf_run(bad, t(ys), spec, be)  # queued: no error yet
+    with pytest.raises(psk.NotPositiveDefinite):
+        be.sync()
+    be.sync()  # the error word was reset
+    _ = rts_check = port.rts_run(m, ys)
+    assert max_rel_err(outs[0].mean, outs[0].cov, *rts_check) < TOL64
+
+
 def test_fast_many_seeds_acceptance(psk, fast, port):
     """acceptance criterion 3 shape (test_acceptance.cpp:102-127)."""
     for seed in range(10):
