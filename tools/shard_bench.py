@@ -48,6 +48,7 @@ def main() -> None:
         m = model(n_in)
         ys = torch.as_tensor(ys_all[lo:hi + 1], device=dev)
         be = psk.CudaBackend(0)
+        be.set_option("async", 1)  # as bench.py's timed region
         from paper_2511_10363_b200.distributed import shard_flags
         eng = CudaShardEngine(be, m, ys, shard_flags(rank, G), hi - lo)
 
@@ -79,6 +80,8 @@ def main() -> None:
         mp = model(hi - lo)
         ysp = torch.as_tensor(ys_all[lo:hi], device=dev)
         bp = psk.CudaBackend(0)
+        bp.set_option("async", 1)
+        bp.set_stream(torch.cuda.current_stream())  # the events' stream
         for _ in range(3):
             psk.prts_run(mp, ysp, spec, bp)
         torch.cuda.synchronize()
