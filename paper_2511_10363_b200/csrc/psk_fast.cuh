@@ -334,19 +334,6 @@ __device__ __forceinline__ void kf_update(Vec<S, NX>& x, Mat<S, NX, NX>& P,
   P = o;
 }
 
-// Kalman prediction (kalman_seq.hpp:36-56) with (F, u, Q) of index k
-template <typename S, int NX>
-__device__ __forceinline__ void kf_predict(Vec<S, NX>& x, Mat<S, NX, NX>& P,
-                                           const ModelView<S>& m,
-                                           long long k) {
-  const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(k));
-  const Vec<S, NX> u = load<S, NX, 1>(m.U(k));
-  const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(k));
-  x = mul_add(F, x, u);
-  const Mat<S, NX, NX> fp = mul(F, P);
-  P = mul_nt_sym_add(fp, F, Q);
-}
-
 // Conditional update of a filter aggregate: the predicted conditional
 // (A, b, C) of x_k given the chunk-start state is updated with y_k and the
 // likelihood information (eta, J) of the chunk-start state is accumulated.
@@ -384,61 +371,6 @@ __device__ __forceinline__ void cond_update(FElem<S, NX>& e,
   e.C = o;
 }
 
-// Filtering element of 0-based step k >= 1 (k = 0 absorbs the prior and is
-// handled in state form by the callers).
-template <typename S, int NX, int NY>
-__device__ __forceinline__ FElem<S, NX> make_filter_elem(const ModelView<S>& m,
-                                                         long long k,
-                                                         unsigned& err) {
-  FElem<S, NX> e;
-  e.A = load<S, NX, NX>(m.F(k));
-  e.b = load<S, NX, 1>(m.U(k));
-  e.C = load<S, NX, NX>(m.Q(k));
-  e.eta = zeros<S, NX, 1>();
-  e.J = zeros<S, NX, NX>();
-  cond_update(e, load_meas<S, NX, NY>(m, k), err);
-  return e;
-}
-
-// Smoothing element of 0-based step i (kalman_elems.hpp:151-193), from the
-// filtered (x, P)_i and the transition (F, Q, u) of index i+1.
-template <typename S, int NX>
-__device__ __forceinline__ SElem<S, NX> make_smoother_elem(
-    const ModelView<S>& m, long long i, const Vec<S, NX>& x,
-    const Mat<S, NX, NX>& P, unsigned& err) {
-  SElem<S, NX> e;
-  if (i == m.last_step) {  // a_T = (0, x_T, P_T), kalman_elems.hpp:158-163
-    e.E = zeros<S, NX, NX>();
-    e.g = x;
-    e.L = P;
-    return e;
-  }
-  const Mat<S, NX, NX> F = load<S, NX, NX>(m.F(i + 1));
-  const Mat<S, NX, NX> Q = load<S, NX, NX>(m.Q(i + 1));
-  const Vec<S, NX> u = load<S, NX, 1>(m.U(i + 1));
-  const Mat<S, NX, NX> fp = mul(F, P);
-  const Mat<S, NX, NX> pp = mul_nt_sym_add(fp, F, Q);
-  const Chol<S, NX> ch = cholesky(pp, err);
-  const Mat<S, NX, NX> et = chol_solve(ch, fp);  // E^T
-  e.E = trans(et);
-  const Vec<S, NX> fx = mul_add(F, x, u);
-  e.g = sub_mul(x, e.E, fx);
-  // L = P - E F P = P - Et^T FP (symmetric)
-  Mat<S, NX, NX> o;
-#pragma unroll
-  for (int a = 0; a < NX; ++a)
-#pragma unroll
-    for (int b = a; b < NX; ++b) {
-      S acc = P.a[a][b];
-#pragma unroll
-      for (int k = 0; k < NX; ++k) acc = sfma(-et.a[k][a], fp.a[k][b], acc);
-      o.a[a][b] = acc;
-      o.a[b][a] = acc;
-    }
-  e.L = o;
-  return e;
-}
-
 template <typename S, int NX>
 __device__ __forceinline__ void store_state(S* mean, S* cov, long long k,
                                             const Vec<S, NX>& x,
@@ -446,14 +378,6 @@ __device__ __forceinline__ void store_state(S* mean, S* cov, long long k,
   store(mean + k * NX, x);
   store(cov + k * NX * NX, P);
 }
-template <typename S, int NX>
-__device__ __forceinline__ void load_state(const S* mean, const S* cov,
-                                           long long k, Vec<S, NX>& x,
-                                           Mat<S, NX, NX>& P) {
-  x = load<S, NX, 1>(mean + k * NX);
-  P = load<S, NX, NX>(cov + k * NX * NX);
-}
-
 // Reduced Lemma-1 combine of a filtered state (an element with A = 0,
 // b = x, C = P) with an element e:  M = I + P J_e,
 // x' = A_e M^-1 (x + P eta_e) + b_e,  P' = A_e M^-1 P A_e^T + C_e.
@@ -636,21 +560,6 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
     __syncthreads();
     if (data) ++it;
   }
-}
-
-// Filtering element of step k from its staged inputs (make_filter_element,
-// kalman_elems.hpp:97-147, k > 1)
-template <typename S, int NX, int NY>
-__device__ __forceinline__ FElem<S, NX> make_filter_elem(const FilterStage<S, NX, NY>& in,
-                                                         unsigned& err) {
-  FElem<S, NX> e;
-  e.A = in.F();
-  e.b = in.u();
-  e.C = in.Q();
-  e.eta = zeros<S, NX, 1>();
-  e.J = zeros<S, NX, NX>();
-  cond_update(e, in.meas(), err);
-  return e;
 }
 
 // Smoothing element of step i from the filtered (x, P)_i and the transition

@@ -208,22 +208,6 @@ __device__ __forceinline__ Mat<S, R, C> mul_tn(const Mat<S, K, R>& x,
     }
   return o;
 }
-// x y^T
-template <typename S, int R, int K, int C>
-__device__ __forceinline__ Mat<S, R, C> mul_nt(const Mat<S, R, K>& x,
-                                               const Mat<S, C, K>& y) {
-  Mat<S, R, C> o;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      S acc = x.a[i][0] * y.a[j][0];
-#pragma unroll
-      for (int k = 1; k < K; ++k) acc = sfma(x.a[i][k], y.a[j][k], acc);
-      o.a[i][j] = acc;
-    }
-  return o;
-}
 // symmetric result x y^T + z, upper triangle computed and mirrored (the
 // mirror replaces the reference's mat_symmetrize, mat.hpp:124-136)
 template <typename S, int N, int K>
@@ -238,24 +222,6 @@ __device__ __forceinline__ Mat<S, N, N> mul_nt_sym_add(const Mat<S, N, K>& x,
       S acc = z.a[i][j];
 #pragma unroll
       for (int k = 0; k < K; ++k) acc = sfma(x.a[i][k], y.a[j][k], acc);
-      o.a[i][j] = acc;
-      o.a[j][i] = acc;
-    }
-  return o;
-}
-// symmetric z - x y^T (upper triangle, mirrored)
-template <typename S, int N, int K>
-__device__ __forceinline__ Mat<S, N, N> sub_mul_nt_sym(const Mat<S, N, N>& z,
-                                                       const Mat<S, N, K>& x,
-                                                       const Mat<S, N, K>& y) {
-  Mat<S, N, N> o;
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = i; j < N; ++j) {
-      S acc = z.a[i][j];
-#pragma unroll
-      for (int k = 0; k < K; ++k) acc = sfma(-x.a[i][k], y.a[j][k], acc);
       o.a[i][j] = acc;
       o.a[j][i] = acc;
     }
