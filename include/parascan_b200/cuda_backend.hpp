@@ -15,7 +15,12 @@
 // scan.hpp:28-30).
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -49,8 +54,82 @@ inline void check(int st) {
 }
 }  // namespace psk_detail
 
+namespace psk_detail {
+
+// ---- host marshalling ------------------------------
+// The reference containers are per-step heap objects (lgssm.hpp:29-45,
+// GaussianStats lgssm.hpp:18-21): packing them into the C-ABI's per-field
+// arrays and building the output vector are memory-bound host loops that the
+// reference runs on one thread (probe: 5.7 s pack + 1.8 s unpack at 2^22).
+// Here both are split over the host cores by step range, and the packed
+// inputs / raw outputs live in PINNED buffers owned by the backend (reused
+// across calls), so the device copies run at full PCIe speed.
+
+// worker count: $PSK_HOST_THREADS, else the hardware concurrency
+inline unsigned host_threads() {
+  if (const char* e = std::getenv("PSK_HOST_THREADS")) {
+    const long v = std::strtol(e, nullptr, 10);
+    if (v >= 1) return unsigned(v);
+  }
+  const unsigned h = std::thread::hardware_concurrency();
+  return h ? h : 1;
+}
+
+// fn(lo, hi) over [0, n) in contiguous ranges of at least `grain` steps
+template <class Fn>
+void parallel_for(std::size_t n, std::size_t grain, Fn&& fn) {
+  const std::size_t want = grain ? (n + grain - 1) / grain : 1;
+  const std::size_t nt = std::max<std::size_t>(1, std::min<std::size_t>(host_threads(), want));
+  if (nt <= 1) {
+    fn(std::size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  std::exception_ptr err;
+  std::mutex mu;
+  auto body = [&](std::size_t i) {
+    try {
+      fn(n * i / nt, n * (i + 1) / nt);
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!err) err = std::current_exception();
+    }
+  };
+  for (std::size_t i = 1; i < nt; ++i) pool.emplace_back(body, i);
+  body(0);
+  for (auto& t : pool) t.join();
+  if (err) std::rethrow_exception(err);
+}
+
+// A growable pinned host buffer (psk_host_alloc); contents are scratch.
+class Pinned {
+ public:
+  Pinned() = default;
+  ~Pinned() { psk_host_free(p_); }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  void* reserve(std::size_t bytes) {
+    if (bytes > cap_) {
+      psk_host_free(p_);
+      p_ = nullptr;
+      cap_ = 0;
+      check(psk_host_alloc(&p_, bytes));
+      cap_ = bytes;
+    }
+    return p_;
+  }
+
+ private:
+  void* p_ = nullptr;
+  std::size_t cap_ = 0;
+};
+
+}  // namespace psk_detail
+
 // The Backend& executor slot (backend.hpp:39-44) filled by a psk context on
 // one CUDA device.  Host closures cannot run on the device, so run() throws.
+// The backend also owns the pinned staging of the marshalling layer.
 class CudaBackend final : public Backend {
  public:
   explicit CudaBackend(int device = 0, int mode = PSK_MODE_FAST, int chunk = 0) {
@@ -67,9 +146,12 @@ class CudaBackend final : public Backend {
   }
   unsigned workers() const override { return 1; }
   psk_ctx* ctx() const { return ctx_; }
+  psk_detail::Pinned& staging_in() { return in_; }
+  psk_detail::Pinned& staging_out() { return out_; }
 
  private:
   psk_ctx* ctx_ = nullptr;
+  psk_detail::Pinned in_, out_;
 };
 
 namespace psk_detail {
@@ -81,74 +163,98 @@ constexpr int dtype_of() {
   return std::is_same_v<S, double> ? PSK_F64 : PSK_F32;
 }
 
-// Lgssm<S> (per-step std::vector<Mat>) -> dense per-step host arrays
+// Lgssm<S> (per-step std::vector<Mat>) -> per-field dense arrays in the
+// backend's pinned input buffer (one field after another, 16-byte aligned)
 template <typename S>
-struct Packed {
-  std::vector<S> f, u, q, h, d, r, y, m0, p0;
-  psk_model model{};
-};
-
-template <typename S, class M>
-void pack_mats(std::vector<S>& out, const std::vector<M>& src, std::size_t block) {
-  out.resize(src.size() * block);
-  for (std::size_t k = 0; k < src.size(); ++k)
-    for (std::size_t i = 0; i < block; ++i)
-      out[k * block + i] = src[k].view().d[i];
-}
-
-template <typename S>
-Packed<S> pack(const Lgssm<S>& m, const Measurements<S>& ys) {
-  Packed<S> p;
-  const std::size_t nx = std::size_t(m.nx), ny = std::size_t(m.ny);
-  if (m.f.size() != m.t || m.u.size() != m.t || m.q.size() != m.t || m.h.size() != m.t ||
-      m.d.size() != m.t || m.r.size() != m.t || ys.size() != m.t)
+psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
+  const std::size_t nx = std::size_t(m.nx), ny = std::size_t(m.ny), t = m.t;
+  if (m.f.size() != t || m.u.size() != t || m.q.size() != t || m.h.size() != t ||
+      m.d.size() != t || m.r.size() != t || ys.size() != t)
     throw DimensionMismatch("model / measurement length");
-  pack_mats(p.f, m.f, nx * nx);
-  pack_mats(p.u, m.u, nx);
-  pack_mats(p.q, m.q, nx * nx);
-  pack_mats(p.h, m.h, ny * nx);
-  pack_mats(p.d, m.d, ny);
-  pack_mats(p.r, m.r, ny * ny);
-  pack_mats(p.y, ys, ny);
-  p.m0.assign(m.prior_mean.view().d, m.prior_mean.view().d + nx);
-  p.p0.assign(m.prior_cov.view().d, m.prior_cov.view().d + nx * nx);
-  psk_model& md = p.model;
-  md.t = m.t;
+  const std::size_t blk[9] = {nx * nx, nx, nx * nx, ny * nx, ny, ny * ny, ny, nx, nx * nx};
+  std::size_t off[9], total = 0;
+  const std::size_t align = 16 / sizeof(S);
+  for (int i = 0; i < 9; ++i) {
+    off[i] = total;
+    const std::size_t n = i < 7 ? blk[i] * t : blk[i];
+    total += (n + align - 1) / align * align;
+  }
+  S* base = static_cast<S*>(buf.reserve(sizeof(S) * (total ? total : 1)));
+  parallel_for(t, 1 << 14, [&](std::size_t lo, std::size_t hi) {
+    auto put = [&](int i, const auto& src) {
+      S* dst = base + off[i];
+      const std::size_t b = blk[i];
+      for (std::size_t k = lo; k < hi; ++k) std::memcpy(dst + k * b, src[k].view().d, sizeof(S) * b);
+    };
+    put(0, m.f);
+    put(1, m.u);
+    put(2, m.q);
+    put(3, m.h);
+    put(4, m.d);
+    put(5, m.r);
+    put(6, ys);
+  });
+  std::memcpy(base + off[7], m.prior_mean.view().d, sizeof(S) * nx);
+  std::memcpy(base + off[8], m.prior_cov.view().d, sizeof(S) * nx * nx);
+  psk_model md{};
+  md.t = t;
   md.nx = m.nx;
   md.ny = m.ny;
   md.dtype = dtype_of<S>();
   md.space = PSK_HOST;
-  md.f = p.f.data(); md.u = p.u.data(); md.q = p.q.data(); md.h = p.h.data();
-  md.d = p.d.data(); md.r = p.r.data(); md.y = p.y.data();
+  const void** fp[7] = {&md.f, &md.u, &md.q, &md.h, &md.d, &md.r, &md.y};
+  for (int i = 0; i < 7; ++i) *fp[i] = base + off[i];
   md.f_stride = md.u_stride = md.q_stride = md.h_stride = md.d_stride =
       md.r_stride = md.y_stride = -1;
-  md.prior_mean = p.m0.data();
-  md.prior_cov = p.p0.data();
-  return p;
+  md.prior_mean = base + off[7];
+  md.prior_cov = base + off[8];
+  return md;
 }
 
+// raw outputs mean[T][nx], cov[T][nx][nx] -> vector<GaussianStats<S>>; every
+// step's Vec / Mat is allocated by the worker that fills it
 template <typename S>
-std::vector<GaussianStats<S>> unpack(const std::vector<S>& mean,
-                                     const std::vector<S>& cov, std::size_t t, int nx) {
-  std::vector<GaussianStats<S>> out;
-  out.reserve(t);
-  for (std::size_t k = 0; k < t; ++k) {
-    GaussianStats<S> g{Vec<S>(nx), Mat<S>(nx, nx)};
-    for (int i = 0; i < nx; ++i) g.mean[i] = mean[k * nx + i];
-    std::memcpy(g.cov.data(), cov.data() + k * nx * nx, sizeof(S) * nx * nx);
-    out.push_back(std::move(g));
-  }
+std::vector<GaussianStats<S>> unpack(const S* mean, const S* cov, std::size_t t, int nx) {
+  std::vector<GaussianStats<S>> out(t);
+  const std::size_t n = std::size_t(nx);
+  parallel_for(t, 1 << 13, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t k = lo; k < hi; ++k) {
+      GaussianStats<S>& g = out[k];
+      g.mean = Vec<S>(nx);
+      g.cov = Mat<S>(nx, nx);
+      std::memcpy(g.mean.view().d, mean + k * n, sizeof(S) * n);
+      std::memcpy(g.cov.data(), cov + k * n * n, sizeof(S) * n * n);
+    }
+  });
   return out;
 }
 
+inline void check_dims(int nx, int ny) {
+  if (nx < 1 || nx > kMaxDim || ny < 1 || ny > kMaxDim) throw DimensionMismatch("mat dims");
+}
+
+// vector<GaussianStats> outputs: raw results land in the pinned output buffer
 template <typename S, class F>
-std::vector<GaussianStats<S>> call(const Lgssm<S>& m, const Measurements<S>& ys, F&& f) {
-  if (m.nx < 1 || m.nx > kMaxDim || m.ny < 1 || m.ny > kMaxDim)
-    throw DimensionMismatch("mat dims");
-  Packed<S> p = pack(m, ys);
-  std::vector<S> mean(m.t * std::size_t(m.nx) + 1), cov(m.t * std::size_t(m.nx * m.nx) + 1);
-  check(f(p.model, mean.data(), cov.data()));
+std::vector<GaussianStats<S>> call(const Lgssm<S>& m, const Measurements<S>& ys,
+                                   CudaBackend& be, F&& f) {
+  check_dims(m.nx, m.ny);
+  const psk_model md = pack(m, ys, be.staging_in());
+  const std::size_t nm = m.t * std::size_t(m.nx), nc = nm * std::size_t(m.nx);
+  const std::size_t mb = (sizeof(S) * nm + 15) / 16 * 16;
+  char* o = static_cast<char*>(be.staging_out().reserve(mb + sizeof(S) * nc + 16));
+  S* mean = reinterpret_cast<S*>(o);
+  S* cov = reinterpret_cast<S*>(o + mb);
+  check(f(md, mean, cov));
   return unpack(mean, cov, m.t, m.nx);
+}
+
+// caller-owned SoA outputs (mean[T][nx], cov[T][nx][nx], host memory)
+template <typename S, class F>
+void call_into(const Lgssm<S>& m, const Measurements<S>& ys, CudaBackend& be, S* mean, S* cov,
+               F&& f) {
+  check_dims(m.nx, m.ny);
+  const psk_model md = pack(m, ys, be.staging_in());
+  check(f(md, mean, cov));
 }
 
 }  // namespace psk_detail
@@ -157,7 +263,7 @@ std::vector<GaussianStats<S>> call(const Lgssm<S>& m, const Measurements<S>& ys,
 template <typename S>
 std::vector<GaussianStats<S>> pkf_run(const Lgssm<S>& m, const Measurements<S>& ys,
                                       const ScanSpec& spec, CudaBackend& be) {
-  return psk_detail::call(m, ys, [&](const psk_model& md, S* mean, S* cov) {
+  return psk_detail::call(m, ys, be, [&](const psk_model& md, S* mean, S* cov) {
     return psk_pkf(be.ctx(), &md, int(spec.alg), spec.sengupta_n, mean, cov);
   });
 }
@@ -166,7 +272,7 @@ std::vector<GaussianStats<S>> pkf_run(const Lgssm<S>& m, const Measurements<S>& 
 template <typename S>
 std::vector<GaussianStats<S>> prts_run(const Lgssm<S>& m, const Measurements<S>& ys,
                                        const ScanSpec& spec, CudaBackend& be) {
-  return psk_detail::call(m, ys, [&](const psk_model& md, S* mean, S* cov) {
+  return psk_detail::call(m, ys, be, [&](const psk_model& md, S* mean, S* cov) {
     return psk_prts(be.ctx(), &md, int(spec.alg), spec.sengupta_n, mean, cov);
   });
 }
@@ -176,9 +282,36 @@ template <typename S>
 std::vector<GaussianStats<S>> ptfs_run(const Lgssm<S>& m, const Measurements<S>& ys,
                                        const ScanSpec& spec, CudaBackend& be_fwd,
                                        CudaBackend& be_bwd, int devices = 1) {
-  return psk_detail::call(m, ys, [&](const psk_model& md, S* mean, S* cov) {
+  return psk_detail::call(m, ys, be_fwd, [&](const psk_model& md, S* mean, S* cov) {
     return psk_ptfs(be_fwd.ctx(), be_bwd.ctx(), devices, &md, int(spec.alg),
                     spec.sengupta_n, mean, cov);
+  });
+}
+
+// SoA-output overloads (no reference counterpart):
+// the smoothed / filtered stats go straight into caller-owned host arrays
+// mean[T][nx] and cov[T][nx][nx] (pinned memory copies at full speed) --
+// no per-step heap objects are built.
+template <typename S>
+void pkf_run(const Lgssm<S>& m, const Measurements<S>& ys, const ScanSpec& spec,
+             CudaBackend& be, S* mean, S* cov) {
+  psk_detail::call_into(m, ys, be, mean, cov, [&](const psk_model& md, S* mo, S* co) {
+    return psk_pkf(be.ctx(), &md, int(spec.alg), spec.sengupta_n, mo, co);
+  });
+}
+template <typename S>
+void prts_run(const Lgssm<S>& m, const Measurements<S>& ys, const ScanSpec& spec,
+              CudaBackend& be, S* mean, S* cov) {
+  psk_detail::call_into(m, ys, be, mean, cov, [&](const psk_model& md, S* mo, S* co) {
+    return psk_prts(be.ctx(), &md, int(spec.alg), spec.sengupta_n, mo, co);
+  });
+}
+template <typename S>
+void ptfs_run(const Lgssm<S>& m, const Measurements<S>& ys, const ScanSpec& spec,
+              CudaBackend& be_fwd, CudaBackend& be_bwd, int devices, S* mean, S* cov) {
+  psk_detail::call_into(m, ys, be_fwd, mean, cov, [&](const psk_model& md, S* mo, S* co) {
+    return psk_ptfs(be_fwd.ctx(), be_bwd.ctx(), devices, &md, int(spec.alg), spec.sengupta_n,
+                    mo, co);
   });
 }
 

@@ -184,6 +184,14 @@ int psk_last_profile(psk_ctx* ctx, const char** names, float* ms, int cap);
 /* Number of this library's kernels launched by the last call. */
 int64_t psk_last_launch_count(psk_ctx* ctx);
 
+/* Pinned (page-locked, portable) host memory for HOST-space models and
+ * outputs: the input / output copies of a call then run at full PCIe speed
+ * instead of staging through pageable buffers.  The C++ shim's marshalling
+ * (include/parascan_b200/cuda_backend.hpp) packs the reference containers
+ * into such a buffer.  bytes = 0 yields NULL; psk_host_free(NULL) is a no-op. */
+int psk_host_alloc(void** p, size_t bytes);
+int psk_host_free(void* p);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* psk_last_error(void);
 /* Library version string. */

@@ -62,6 +62,34 @@ int main() {
     std::printf("nx=%d ny=%d alg=decoupled_lookback prts %.3e\n", d[0], d[1], ed);
     if (!(ed < 1e-9)) ++bad;
   }
+  // SoA-output overloads (caller-owned arrays) == the vector<GaussianStats> path
+  {
+    const Lgssm<double> m = gen_model(21, 4, 2, 3000);
+    const Measurements<double> ys = simulate_data(m, 22);
+    const ScanSpec spec{kDecoupledLookback, 1};
+    const auto v = prts_run(m, ys, spec, gpu);
+    std::vector<double> mean(m.t * 4), cov(m.t * 16);
+    prts_run(m, ys, spec, gpu, mean.data(), cov.data());
+    double e = 0;
+    for (std::size_t k = 0; k < m.t; ++k) {
+      for (int i = 0; i < 4; ++i) e = std::fmax(e, std::fabs(mean[k * 4 + i] - v[k].mean[i]));
+      for (int i = 0; i < 16; ++i) e = std::fmax(e, std::fabs(cov[k * 16 + i] - v[k].cov.data()[i]));
+    }
+    std::printf("SoA-output prts vs vector prts: max |diff| %.3e\n", e);
+    if (e != 0.0) ++bad;
+    // f32 through the shim against the reference's f32 PoolBackend result
+    const auto m32 = convert_model<float>(m);
+    const auto ys32 = convert_measurements<float>(ys);
+    const auto g32 = prts_run(m32, ys32, ScanSpec{ScanAlg::InplaceLaFi, 1}, gpu);
+    const auto r32 = prts_run(m32, ys32, ScanSpec{ScanAlg::InplaceLaFi, 1}, pool);
+    double e32 = 0;
+    for (std::size_t k = 0; k < m.t; ++k)
+      for (int i = 0; i < 16; ++i)
+        e32 = std::fmax(e32, std::fabs(double(g32[k].cov.data()[i]) - r32[k].cov.data()[i]) /
+                                 (1 + std::fabs(r32[k].cov.data()[i])));
+    std::printf("f32 prts cov vs reference f32: %.3e\n", e32);
+    if (!(e32 < 1e-2)) ++bad;  // the reference's f32 gate (bench.hpp rel_err_tolerance)
+  }
   // error behaviour
   {
     Lgssm<double> m = gen_model(3, 4, 2, 50);

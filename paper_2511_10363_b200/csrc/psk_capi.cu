@@ -798,6 +798,28 @@ int psk_fold_smoother(psk_ctx* c, int dtype, int nx, const void* elems, int coun
   return fold_entry(c, 1, dtype, nx, elems, count, out);
 }
 
+int psk_host_alloc(void** p, size_t bytes) {
+  if (!p) return fail(PSK_E_ARG, "null pointer out");
+  *p = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(PSK_E_CUDA, std::string("no CUDA device: ") + cuda_msg(e));
+  if (bytes == 0) return PSK_OK;
+  e = cudaHostAlloc(p, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(PSK_E_ALLOC, std::string("pinned host allocation: ") + cuda_msg(e));
+  }
+  return PSK_OK;
+}
+
+int psk_host_free(void* p) {
+  if (!p) return PSK_OK;
+  const cudaError_t e = cudaFreeHost(p);
+  return e == cudaSuccess ? PSK_OK : fail(PSK_E_CUDA, std::string("cudaFreeHost: ") + cuda_msg(e));
+}
+
 const char* psk_last_error(void) { return g_last_error.c_str(); }
 const char* psk_version(void) { return "psk-b200 0.1.0 (sm_100a)"; }
 
