@@ -10,7 +10,10 @@ prts_run over the whole series.
   value  -- device-resident throughput: inputs already in HBM, outputs to HBM,
             CUDA events on the library's stream, max over ranks;
   e2e    -- the same call through the public API with pinned HOST buffers:
-            H2D of all inputs and D2H of all outputs inside the timed region.
+            H2D of all inputs and D2H of all outputs inside the timed region,
+            a stream of series on two async contexts so one series' input
+            copy overlaps the previous one's result copy (sync_value: one
+            synchronous call at a time).
 
 With --gpus N > 1 (torchrun, one rank per GPU) the time axis is sharded: each
 rank filters / smooths its contiguous chunk, the shard aggregates are
@@ -388,7 +391,7 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
         out = psk.prts_run(m, ys, spec, be, out=res)
         float(out.mean[-1, 0])  # the result is on the host
         ts.append(time.perf_counter() - t0)
-    sec = sum(ts) / len(ts)
+    sec_sync = sum(ts) / len(ts)
     # where an end-to-end call goes (CUDA events of one profiled call)
     be.set_profile(True)
     psk.prts_run(m, ys, spec, be, out=res)
@@ -397,14 +400,45 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
     br = {"h2d_inputs": sum(ms for n, ms in prof if n == "h2d_inputs"),
           "kernels": sum(ms for n, ms in prof if not n.startswith(("h2d", "d2h"))),
           "d2h_outputs": sum(ms for n, ms in prof if n == "d2h_outputs")}
+    # A stream of series through the same API: two contexts in "async" mode
+    # take alternate steps, so step i's input copy (H2D) runs while step i-1
+    # computes and copies its result back (D2H) -- the two PCIe directions
+    # overlap.  Every step still copies its own inputs in and its result out,
+    # and the host reads each result after that step's psk_sync.
+    bes = [be, psk.CudaBackend(local, mode="fast", chunk=args.chunk)]
+    outs = [res, psk.GaussianStats(torch.empty((T, 4), dtype=tdt, pin_memory=True),
+                                   torch.empty((T, 4, 4), dtype=tdt, pin_memory=True))]
+    for b in bes:
+        b.set_option("async", 1)
+    for j in range(2):  # warm-up (allocations of the second context)
+        psk.prts_run(m, ys, spec, bes[j], out=outs[j])
+    for b in bes:
+        b.sync()
+    psteps = max(4, min(args.steps, 8))
+    t0 = time.perf_counter()
+    for i in range(psteps):
+        j = i % 2
+        if i >= 2:
+            bes[j].sync()
+            float(outs[j].mean[-1, 0])  # step i-2's result, on the host
+        psk.prts_run(m, ys, spec, bes[j], out=outs[j])
+    for i in range(psteps - 2, psteps):
+        bes[i % 2].sync()
+        float(outs[i % 2].mean[-1, 0])
+    sec = (time.perf_counter() - t0) / psteps
+    for b in bes:
+        b.set_option("async", 0)
     return {"value": T / sec, "unit": "time-steps/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "timer": "wall clock around the synchronous API call",
+            "d2h_bytes_per_step": int(d2h), "steps": psteps,
+            "timer": "wall clock over the step loop (host reads every step's result)",
+            "pipelining": "2 contexts, async API: step i's H2D overlaps step i-1's "
+                          "kernels + D2H",
+            "sync_value": T / sec_sync,
+            "sync_note": "one synchronous call at a time (H2D, kernels, D2H in series)",
             "breakdown_ms": {k: round(v, 2) for k, v in br.items()},
             "pcie_note": "pinned copies: H2D ~55.6 GB/s, D2H ~55.0 GB/s on this box "
-                         "(tools/pcie.py); PRTS cannot overlap them (every smoothed output "
-                         "depends on every input)"}
-
+                         "(tools/pcie.py); within one PRTS call they cannot overlap (every "
+                         "smoothed output depends on every input), across calls they do"}
 
 if __name__ == "__main__":
     main()

@@ -106,6 +106,8 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
  *               queued on the context's stream (outputs valid when the stream
  *               completes; errors are reported by psk_sync); default 0 =
  *               synchronous, like the reference's drivers
+ *   "batch_streams"  sub-streams of psk_pkf_batch / psk_prts_batch (1..64,
+ *               default 4)
  *   "shard_async"  1: the shard phases before psk_shard_smoother_finish and
  *               the folds return without synchronising the stream (errors
  *               are reported by the smoother finish); default 0
@@ -134,6 +136,20 @@ int psk_prts(psk_ctx* ctx, const psk_model* model, int alg,
 int psk_ptfs(psk_ctx* ctx_fwd, psk_ctx* ctx_bwd, int devices,
              const psk_model* model, int alg, uint64_t sengupta_n, void* mean,
              void* cov);
+
+/* Batches of independent series (no reference counterpart; SURVEY.md 8(f)
+ * row 2, BASELINE configs[4]): series i is models[i] with outputs means[i],
+ * covs[i] (each series its own T, dims, dtype, space, strides -- e.g.
+ * time-invariant per-series models with stride-0 fields).  Every series is
+ * validated before any work is queued; the series then run on
+ * "batch_streams" (option, default 4) sub-streams of the context's stream,
+ * so series too short to fill the GPU alone overlap.  Synchronous unless the
+ * context is in async mode; on a failure the first failing series' status is
+ * returned (series after it are not run). */
+int psk_pkf_batch(psk_ctx* ctx, const psk_model* models, int count, int alg,
+                  uint64_t sengupta_n, void* const* means, void* const* covs);
+int psk_prts_batch(psk_ctx* ctx, const psk_model* models, int count, int alg,
+                   uint64_t sengupta_n, void* const* means, void* const* covs);
 
 /* ---- time-sharded PRTS: one process per GPU (paper_2511_10363_b200/
  * distributed.py).  A shard is the steps [lo, hi) of a

@@ -8,10 +8,12 @@ backend object.
 """
 from .api import (ContractViolation, CudaBackend, CudaError, DimensionMismatch,
                   GaussianStats, Lgssm, NotPositiveDefinite, ScanAlg, ScanSpec,
-                  SingularMatrix, pkf_run, prts_run, ptfs_run, to_string)
+                  SingularMatrix, pkf_run, pkf_run_batch, prts_run, prts_run_batch,
+                  ptfs_run, to_string)
 
 __all__ = [
     "ContractViolation", "CudaBackend", "CudaError", "DimensionMismatch",
     "GaussianStats", "Lgssm", "NotPositiveDefinite", "ScanAlg", "ScanSpec",
-    "SingularMatrix", "pkf_run", "prts_run", "ptfs_run", "to_string",
+    "SingularMatrix", "pkf_run", "pkf_run_batch", "prts_run", "prts_run_batch", "ptfs_run",
+    "to_string",
 ]

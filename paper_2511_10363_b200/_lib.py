@@ -71,6 +71,10 @@ SIGNATURES = {
     "psk_last_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p),
                                    C.POINTER(C.c_float), C.c_int]),
     "psk_last_launch_count": (C.c_int64, [C.c_void_p]),
+    "psk_pkf_batch": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int, C.c_int,
+                                C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "psk_prts_batch": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int, C.c_int,
+                                 C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "psk_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "psk_host_free": (C.c_int, [C.c_void_p]),
     "psk_last_error": (C.c_char_p, []),

@@ -383,3 +383,41 @@ def ptfs_run(m: Lgssm, ys: Any, spec: ScanSpec, be_fwd: CudaBackend,
              out: GaussianStats | None = None) -> GaussianStats:
     """Parallel two-filter smoother, Alg. 7 (kalman_par.hpp:207-238)."""
     return _run("ptfs", m, ys, spec, be_fwd, be_bwd, devices, out=out)
+
+
+def _run_batch(entry: str, models: list[Lgssm], ys_list: list[Any], spec: ScanSpec,
+               be: CudaBackend, outs: list[GaussianStats] | None = None) -> list[GaussianStats]:
+    if len(models) != len(ys_list) or (outs is not None and len(outs) != len(models)):
+        raise DimensionMismatch("batch lengths differ")
+    mks, res = [], []
+    for i, (m, ys) in enumerate(zip(models, ys_list)):
+        _validate(m)
+        mk = _Marshal(m, ys)
+        if outs is None:
+            mean, cov = mk.outputs()
+        else:
+            mean, cov = outs[i].mean, outs[i].cov
+            if tuple(mean.shape) != (mk.t, mk.nx) or tuple(cov.shape) != (mk.t, mk.nx, mk.nx):
+                raise DimensionMismatch("output buffer shapes")
+        mks.append(mk)
+        res.append(GaussianStats(mean, cov))
+    n = len(mks)
+    arr = (_lib.psk_model * max(n, 1))(*[mk.model for mk in mks])
+    pm = (C.c_void_p * max(n, 1))(*[mks[i]._ptr(res[i].mean) for i in range(n)])
+    pc = (C.c_void_p * max(n, 1))(*[mks[i]._ptr(res[i].cov) for i in range(n)])
+    fn = _lib.lib().psk_pkf_batch if entry == "pkf" else _lib.lib().psk_prts_batch
+    _check(fn(be.handle, arr, n, int(spec.alg), int(spec.sengupta_n), pm, pc))
+    return res
+
+
+def pkf_run_batch(models: list[Lgssm], ys_list: list[Any], spec: ScanSpec, be: CudaBackend,
+                  outs: list[GaussianStats] | None = None) -> list[GaussianStats]:
+    """A batch of independent series through the PKF (psk_pkf_batch): every
+    series validated first, then queued on the context's sub-streams."""
+    return _run_batch("pkf", models, ys_list, spec, be, outs)
+
+
+def prts_run_batch(models: list[Lgssm], ys_list: list[Any], spec: ScanSpec, be: CudaBackend,
+                   outs: list[GaussianStats] | None = None) -> list[GaussianStats]:
+    """A batch of independent series through the PRTS (psk_prts_batch)."""
+    return _run_batch("prts", models, ys_list, spec, be, outs)

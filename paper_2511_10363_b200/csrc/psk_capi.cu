@@ -51,6 +51,10 @@ struct psk_ctx {
   int shard_alg = 6;
   uint64_t shard_sn = 1;
   std::vector<std::pair<const char*, float>> profile;
+  // batched calls: series i runs on sub[i % batch_streams]
+  int batch_streams = 4;
+  std::vector<cudaStream_t> sub;
+  std::vector<cudaEvent_t> sub_ev;  // fork (index 0) / join events
 };
 
 namespace {
@@ -370,6 +374,88 @@ int run_entry(psk_ctx* ctx, const psk_model* m, int method, int alg,
   return PSK_OK;
 }
 
+// A batch of independent series: every series is
+// validated first, then series i is queued on the context's sub-stream
+// i % batch_streams (forked from and joined back into the context's stream),
+// so short series that do not fill the GPU alone run concurrently.  One
+// synchronisation at the end (none in async mode).
+int batch_entry(psk_ctx* ctx, const psk_model* ms, int count, int method, int alg,
+                uint64_t sengupta_n, void* const* means, void* const* covs) {
+  if (count < 0) return fail(PSK_E_ARG, "negative batch count");
+  if (count > 0 && (!ms || !means || !covs)) return fail(PSK_E_ARG, "null batch array");
+  for (int i = 0; i < count; ++i) {
+    const psk_model* m = &ms[i];
+    if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16) return fail(PSK_E_DIM, "mat dims");
+    if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+    if (m->space != PSK_HOST && m->space != PSK_DEVICE) return fail(PSK_E_ARG, "bad space");
+    const int st = check_contract(alg, sengupta_n, m->t);
+    if (st) return st;
+    if (m->t > 0 && (!means[i] || !covs[i])) return fail(PSK_E_ARG, "null output");
+  }
+  if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (count == 0) return PSK_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg(ctx->device);
+  const int k = std::max(1, std::min(count, ctx->batch_streams));
+  while ((int)ctx->sub.size() < k) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(PSK_E_CUDA, "batch stream creation failed");
+    ctx->sub.push_back(s);
+  }
+  while ((int)ctx->sub_ev.size() < k + 1) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return fail(PSK_E_CUDA, "batch event creation failed");
+    ctx->sub_ev.push_back(e);
+  }
+  cudaStream_t main = ctx->stream;
+  const bool prof = ctx->launch.profile;
+  ctx->launch.profile = false;  // event spans across streams are not per-kernel times
+  ctx->launch.err = ctx->d_err;
+  ctx->launch.stream = main;
+  ctx->launch.start(ctx->async != 0);
+  if (!ctx->async) cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), main);
+  cudaEventRecord(ctx->sub_ev[0], main);
+  for (int j = 0; j < k; ++j) cudaStreamWaitEvent(ctx->sub[j], ctx->sub_ev[0], 0);
+  int st = PSK_OK;
+  long long launches = 0;
+  for (int i = 0; i < count && st == PSK_OK; ++i) {
+    ctx->stream = ctx->sub[i % k];
+    ctx->launch.stream = ctx->stream;
+    ctx->launch.launches = 0;
+    const psk_model* m = &ms[i];
+    st = m->dtype == PSK_F64
+             ? run_typed<double>(ctx, m, method, alg, sengupta_n, means[i], covs[i])
+             : run_typed<float>(ctx, m, method, alg, sengupta_n, means[i], covs[i]);
+    launches += ctx->launch.launches;
+    ctx_free_all(ctx);  // stream-ordered on the series' stream
+  }
+  for (int j = 0; j < k; ++j) {
+    cudaEventRecord(ctx->sub_ev[j + 1], ctx->sub[j]);
+    cudaStreamWaitEvent(main, ctx->sub_ev[j + 1], 0);
+  }
+  ctx->stream = main;
+  ctx->launch.stream = main;
+  ctx->launch.launches = launches;
+  ctx->launch.profile = prof;
+  if (st) {
+    cudaStreamSynchronize(main);
+    return st;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("kernel launch: ") + cuda_msg(e));
+  if (ctx->async) return PSK_OK;
+  unsigned herr = 0;
+  cudaMemcpyAsync(&herr, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, main);
+  e = cudaStreamSynchronize(main);
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  ctx->profile.clear();
+  if (herr & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
+  return PSK_OK;
+}
+
 // ---- time-sharded phases --------------------------------------------------
 template <typename S>
 int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
@@ -655,6 +741,8 @@ int psk_destroy(psk_ctx* c) {
     }
     cudaStreamSynchronize(c->stream);
     c->launch.start();  // releases events
+    for (auto s : c->sub) cudaStreamDestroy(s);
+    for (auto e : c->sub_ev) cudaEventDestroy(e);
     cudaFree(c->d_err);
     cudaStreamDestroy(c->own_stream);
   }
@@ -688,6 +776,9 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   } else if (k == "shard_async") {
     if (value != 0 && value != 1) return fail(PSK_E_ARG, "shard_async must be 0 or 1");
     c->shard_async = (int)value;
+  } else if (k == "batch_streams") {
+    if (value < 1 || value > 64) return fail(PSK_E_ARG, "batch_streams must be 1..64");
+    c->batch_streams = (int)value;
   } else if (k == "waves") {
     if (value < 1 || value > 1024) return fail(PSK_E_ARG, "waves must be 1..1024");
     c->waves = (int)value;
@@ -796,6 +887,15 @@ int psk_fold_filter(psk_ctx* c, int dtype, int nx, const void* elems, int count,
 }
 int psk_fold_smoother(psk_ctx* c, int dtype, int nx, const void* elems, int count, void* out) {
   return fold_entry(c, 1, dtype, nx, elems, count, out);
+}
+
+int psk_pkf_batch(psk_ctx* c, const psk_model* ms, int count, int alg, uint64_t sn,
+                  void* const* means, void* const* covs) {
+  return batch_entry(c, ms, count, 0, alg, sn, means, covs);
+}
+int psk_prts_batch(psk_ctx* c, const psk_model* ms, int count, int alg, uint64_t sn,
+                   void* const* means, void* const* covs) {
+  return batch_entry(c, ms, count, 1, alg, sn, means, covs);
 }
 
 int psk_host_alloc(void** p, size_t bytes) {

@@ -150,3 +150,21 @@ def prts_run_sharded(model, ys, spec, be, rank: int, world: int, lo: int, hi: in
         engine = CudaShardEngine(be, model, ys, shard_flags(rank, world), hi - lo)
     mean, cov = prts_sharded(engine, spec, rank, world, hi - lo, group)
     return api.GaussianStats(mean, cov)
+
+
+def batch_shard(n: int, rank: int, world: int) -> range:
+    """BASELINE configs[4] on G GPUs: batch sharding -- rank
+    g runs the contiguous near-equal share of the n independent series; there
+    is no data-path exchange, so scaling is "weak" per series."""
+    lo, hi = shard_range(n, rank, world)
+    return range(lo, hi)
+
+
+def prts_run_batch_sharded(models, ys_list, spec, be, rank: int, world: int):
+    """This rank's share of a batch through one psk_prts_batch call; returns
+    (indices, results)."""
+    from . import api
+
+    idx = batch_shard(len(models), rank, world)
+    res = api.prts_run_batch([models[i] for i in idx], [ys_list[i] for i in idx], spec, be)
+    return idx, res

@@ -127,3 +127,22 @@ def test_cpp_shim_header_compiles(tmp_path):
     p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ROOT / 'include'}",
                         f"-I{ref_inc}", str(src)], capture_output=True, text=True)
     assert p.returncode == 0, p.stderr
+
+
+def test_batch_validation_without_device():
+    """psk_*_batch validate every series (dims, dtype, contracts, outputs)
+    before the context is touched, like the single-series entry points."""
+    from paper_2511_10363_b200 import _lib
+    L = _lib.lib()
+    good = _model(5)
+    bad = _model(5)
+    bad.model.nx = 17
+    arr = (_lib.psk_model * 2)(good.model, bad.model)
+    outs = [np.empty(5 * 17 * 17) for _ in range(2)]
+    pm = (C.c_void_p * 2)(*[C.c_void_p(o.ctypes.data) for o in outs])
+    pc = (C.c_void_p * 2)(*[C.c_void_p(o.ctypes.data) for o in outs])
+    assert L.psk_prts_batch(None, arr, 2, 6, 1, pm, pc) == _lib.PSK_E_DIM
+    arr = (_lib.psk_model * 2)(good.model, good.model)
+    assert L.psk_pkf_batch(None, arr, 2, 5, 3, pm, pc) == _lib.PSK_E_CONTRACT  # SenguptaB n=3
+    assert L.psk_prts_batch(None, arr, -1, 6, 1, pm, pc) == _lib.PSK_E_ARG
+    assert L.psk_prts_batch(None, arr, 2, 6, 1, pm, pc) == _lib.PSK_E_ARG  # null context

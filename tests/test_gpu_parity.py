@@ -363,3 +363,56 @@ def _cast(m, ys, dtype):
     c = lambda a: np.asarray(a, dtype=dtype)
     return Lgssm(f=c(m.f), u=c(m.u), q=c(m.q), h=c(m.h), d=c(m.d), r=c(m.r),
                  prior_mean=c(m.prior_mean), prior_cov=c(m.prior_cov), t=m.t), c(ys)
+
+
+def test_batch_matches_single_calls(psk, gpu, port):
+    """psk_prts_batch / psk_pkf_batch: a batch of heterogeneous series (dims,
+    T, dtype, host / device, time-invariant fields) gives exactly the results
+    of one call per series; short series share the GPU on sub-streams."""
+    import torch
+    be = psk.CudaBackend(gpu)
+    one = psk.CudaBackend(gpu)
+    models, yss = [], []
+    for i, (nx, ny, t) in enumerate([(4, 2, 3000), (2, 1, 1), (4, 2, 257), (8, 4, 700),
+                                     (3, 3, 4096), (4, 2, 50000)]):
+        m, ys = gen(port, 70 + i, nx, ny, t)
+        models.append(m)
+        yss.append(ys)
+    # a time-invariant (stride-0) series on the device, FP32
+    m0, ys0 = gen(port, 90, 4, 2, 2000)
+    c = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float32, device="cuda")  # noqa: E731
+    ti = psk.Lgssm(f=c(m0.f[0]), u=c(m0.u[0]), q=c(m0.q[0]), h=c(m0.h[0]), d=c(m0.d[0]),
+                   r=c(m0.r[0]), prior_mean=c(m0.prior_mean), prior_cov=c(m0.prior_cov), t=2000)
+    models.append(ti)
+    yss.append(torch.as_tensor(ys0, dtype=torch.float32, device="cuda"))
+    spec = psk.ScanSpec(psk.ScanAlg(6))
+    for batch_fn, single_fn in ((psk.prts_run_batch, psk.prts_run),
+                                (psk.pkf_run_batch, psk.pkf_run)):
+        got = batch_fn(models, yss, spec, be)
+        assert be.last_launch_count() > 0
+        for m, ys, g in zip(models, yss, got):
+            w = single_fn(m, ys, spec, one)
+            assert np.array_equal(_np(g.mean), _np(w.mean)) and np.array_equal(_np(g.cov),
+                                                                                _np(w.cov))
+    # and against the oracle for one member
+    got = psk.prts_run_batch(models[:1], yss[:1], spec, be)
+    assert max_rel_err(got[0].mean, got[0].cov, *port.rts_run(models[0], yss[0])) < TOL64
+
+
+def test_batch_errors(psk, gpu, port):
+    """Validation of every series precedes any work; device errors map to the
+    reference exception types."""
+    be = psk.CudaBackend(gpu)
+    m, ys = gen(port, 5, 4, 2, 300)
+    spec = psk.ScanSpec(psk.ScanAlg(6))
+    with pytest.raises(psk.ContractViolation):
+        psk.prts_run_batch([m, scalar_model(0)], [ys, np.zeros((0, 1))], spec, be)
+    bad_r = m.r.copy()
+    bad_r[10] = -1e3 * np.eye(2)
+    bad = psk.Lgssm(f=m.f, u=m.u, q=m.q, h=m.h, d=m.d, r=bad_r, prior_mean=m.prior_mean,
+                    prior_cov=m.prior_cov, t=m.t)
+    with pytest.raises(psk.NotPositiveDefinite):
+        psk.pkf_run_batch([m, bad, m], [ys, ys, ys], spec, be)
+    got = psk.prts_run_batch([m], [ys], spec, be)  # the context is usable after it
+    assert got[0].mean.shape == (300, 4)
+    assert psk.prts_run_batch([], [], spec, be) == []

@@ -12,6 +12,7 @@ stationary marginal N(0, H P_inf H^T + R).  (numpy here: this is a measurement t
 path against the reference restatement is tests/test_gpu_parity.py.)
 
 usage: python tools/config5.py [--batch 64] [--log2t 20] [--dtypes f64,f32]
+                               [--how batch,loop] [--nx 16] [--ny 8]
 """
 from __future__ import annotations
 
@@ -58,6 +59,7 @@ def main() -> None:
     ap.add_argument("--dtypes", default="f64,f32")
     ap.add_argument("--nx", type=int, default=16)
     ap.add_argument("--ny", type=int, default=8)
+    ap.add_argument("--how", default="batch,loop")
     args = ap.parse_args()
     T, nx, ny = 1 << args.log2t, args.nx, args.ny
     dev = torch.device("cuda", 0)
@@ -72,24 +74,33 @@ def main() -> None:
                for F, Q, H, R, _ in seqs]
         ys_ = [c(s[4]) for s in seqs]
         spec = psk.ScanSpec(psk.ScanAlg.DecoupledLookback)
+        outs = [psk.GaussianStats(torch.empty((T, nx), dtype=tdt, device=dev),
+                                  torch.empty((T, nx, nx), dtype=tdt, device=dev))
+                for _ in range(args.batch)]
         with torch.cuda.stream(stream):
-            psk.prts_run(ms_[0], ys_[0], spec, be)  # warm-up
+            psk.prts_run(ms_[0], ys_[0], spec, be, out=outs[0])  # warm-up
+            psk.prts_run_batch(ms_, ys_, spec, be, outs=outs)
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for m, ys in zip(ms_, ys_):
-                psk.prts_run(m, ys, spec, be)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        print(json.dumps({"config": f"nx={nx} ny={ny} T=2^{args.log2t} batch={args.batch} "
-                                    "time-invariant models, PRTS",
-                          "dtype": dts, "ms_total": round(ms, 2),
-                          "ms_per_sequence": round(ms / args.batch, 3),
-                          "steps_per_s": args.batch * T / (ms * 1e-3)}), flush=True)
-
+        for how in args.how.split(","):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                if how == "loop":  # one synchronous call per sequence
+                    for m, ys, o in zip(ms_, ys_, outs):
+                        psk.prts_run(m, ys, spec, be, out=o)
+                else:  # one psk_prts_batch call (sub-streams)
+                    psk.prts_run_batch(ms_, ys_, spec, be, outs=outs)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            print(json.dumps({"config": f"nx={nx} ny={ny} T=2^{args.log2t} batch={args.batch} "
+                                        "time-invariant models, PRTS",
+                              "dtype": dts, "how": how, "ms_total": round(ms, 2),
+                              "ms_per_sequence": round(ms / args.batch, 3),
+                              "steps_per_s": args.batch * T / (ms * 1e-3)}), flush=True)
+        del outs, ms_, ys_  # the FP64 outputs of 64 series at 2^20 hold ~146 GB
+        torch.cuda.empty_cache()
 
 if __name__ == "__main__":
     main()

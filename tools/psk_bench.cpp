@@ -6,7 +6,8 @@
 // sit next to the reference's own CPU rows.
 //
 // It is a reference user's program: the UNMODIFIED reference headers (model
-// generator gen_model / simulate_data, the sequential f64 oracle kf_run /
+// generator gen_model -- run step-parallel by include/parascan_b200/
+// model_gen_par.hpp, bit-identical -- / simulate_data, the sequential f64 oracle kf_run /
 // rts_run, the timing protocol time_run, max_rel_err, CSV writer) plus
 // include/parascan_b200/cuda_backend.hpp.  Built by tools/Makefile into
 // tools/_bin/psk_bench (the reference headers exist only in the build
@@ -51,6 +52,7 @@
 #include "parascan/kalman_seq.hpp"
 #include "parascan/model_gen.hpp"
 #include "parascan_b200/cuda_backend.hpp"
+#include "parascan_b200/model_gen_par.hpp"
 
 using namespace parascan;
 
@@ -318,7 +320,7 @@ int main(int argc, char** argv) {
     std::vector<ResultRow> rows;
     bool gating_failed = false;
     for (std::size_t t : o.t_grid) {
-      const Lgssm<double> m = o.model == "cv" ? cv_model(t) : gen_model(o.seed, o.nx, o.ny, t);
+      const Lgssm<double> m = o.model == "cv" ? cv_model(t) : gen_model_par(o.seed, o.nx, o.ny, t);
       const Measurements<double> ys = simulate_data(m, o.seed + 1);
       const auto kf = kf_run(m, ys);
       const auto rts = rts_run(m, kf);
