@@ -13,11 +13,12 @@
 //      in global scratch;
 //   4. the tile aggregate is published (flag A; tile 0 publishes its inclusive
 //      prefix, flag P, directly);
-//   5. look-back, CTA-parallel: thread i inspects predecessor tile base-i of a
-//      128-wide window, the nearest P in the window bounds it, the window's
-//      aggregates (+ that P) are reduced in time order by a 7-level tree in
-//      shared memory and folded onto the LEFT of the running exclusive prefix
-//      (non-commutative).  Without a P the window slides back by 128 tiles;
+//   5. look-back, CTA-parallel: the flags of 128-wide windows of
+//      predecessors are inspected until the nearest P (inclusive prefix) is
+//      found; the P and the aggregates after it are then split into 128
+//      contiguous blocks, each thread folds its block in time order and a
+//      7-level ordered tree in shared memory reduces the blocks
+//      (non-commutative) -- the exclusive prefix of the tile;
 //   6. the inclusive prefix of the tile is published (flag P) and every thread
 //      re-folds its K elements from (exclusive tile prefix (x) thread
 //      exclusive prefix), writing the inclusive prefixes in place.
@@ -79,14 +80,18 @@ inline long long dlb_tiles(long long n, int per) {
 __host__ __device__ inline size_t dlb_head_bytes(long long ntiles) {
   return 256 + ((size_t)ntiles * 4 + 255) / 256 * 256;
 }
-// state layout: [ticket u32 | pad][flags u32 x ntiles][agg FS x ntiles]
-//               [incl FS x ntiles][thread prefixes FS x ntiles*kDlbThreads]
+// Published tile payloads are AoS, one element per kDlbStride scalars (whole
+// 128-byte lines for FP64): a cache line never mixes tiles, so no line can
+// be cached by a reader before its tile's flag is set.
+constexpr int kDlbStride = 64;
+// state layout: [ticket u32 | pad][flags u32 x ntiles][agg x ntiles (AoS)]
+//               [incl x ntiles (AoS)][thread prefixes FS x ntiles*kDlbThreads]
 // sized for the worst case K = 1 (one element per thread)
 template <typename S, int NX>
 inline size_t dlb_state_bytes(long long n) {
   const long long nt = dlb_tiles(n, 1);
   const size_t fs = (size_t)(3 * NX * NX + 2 * NX);
-  return dlb_head_bytes(nt) + sizeof(S) * fs * (size_t)nt * (2 + kDlbThreads);
+  return dlb_head_bytes(nt) + sizeof(S) * (size_t)nt * (2 * kDlbStride + fs * kDlbThreads);
 }
 
 template <class Ops>
@@ -100,12 +105,14 @@ __global__ void __launch_bounds__(kDlbThreads)
   const ElemBuf<S> gb{buf, n, n, 0};
   unsigned* ticket = reinterpret_cast<unsigned*>(state);
   unsigned* flags = reinterpret_cast<unsigned*>(state + 256);
+  static_assert(Ops::kSize <= kDlbStride, "element wider than the payload stride");
   S* pagg = reinterpret_cast<S*>(state + dlb_head_bytes(ntiles));
-  S* pincl = pagg + (size_t)Ops::kSize * ntiles;
-  S* pthr = pincl + (size_t)Ops::kSize * ntiles;
+  S* pincl = pagg + (size_t)kDlbStride * ntiles;
+  S* pthr = pincl + (size_t)kDlbStride * ntiles;
   const long long thr_cap = ntiles * kDlbThreads;
-  const ElemBuf<S> ab{pagg, ntiles, ntiles, 0};
-  const ElemBuf<S> ib{pincl, ntiles, ntiles, 0};
+  // AoS views: element p at index p * kDlbStride (component stride 1)
+  const ElemBuf<S> ab{pagg, 1, ntiles * kDlbStride, 0};
+  const ElemBuf<S> ib{pincl, 1, ntiles * kDlbStride, 0};
   const ElemBuf<S> tb{pthr, thr_cap, thr_cap, 0};
   constexpr int kExcl = kDlbThreads, kTmp = kDlbThreads + 1;
   __shared__ unsigned s_tile;
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(kDlbThreads)
   constexpr int last = kDlbThreads - 1;
   if (tile > 0) ops.assign(tb, tile * kDlbThreads + t, sb, t);
   if (t == 0) {
-    ops.assign(tile == 0 ? ib : ab, tile, sb, last);
+    ops.assign(tile == 0 ? ib : ab, tile * kDlbStride, sb, last);
     __threadfence();
     st_release(flags + tile, tile == 0 ? 2u : 1u);
     if (tile > 0) ops.assign(sb, kTmp, sb, last);  // keep the tile aggregate
@@ -169,55 +176,61 @@ __global__ void __launch_bounds__(kDlbThreads)
   // tile 0: the tile prefix is the identity; slot t already holds the
   // thread-inclusive prefix (shifted to thread-exclusive below)
   if (tile > 0) {
-    // 5. look-back over windows of kDlbThreads predecessors
-    bool have = false;
+    // 5a. look-back for the nearest predecessor with an inclusive prefix
+    // (flag P), over windows of kDlbThreads flags -- no combines yet; every
+    // predecessor after it has published its aggregate (flag A) by then
+    long long lo = 0;
     long long base = tile - 1;
 #pragma unroll 1
     while (true) {
       if (t == 0) s_stop = kDlbThreads;
       __syncthreads();
       const long long pt = base - t;
-      unsigned f = 0;
       if (pt >= 0) {
+        unsigned f;
         while ((f = ld_acquire(flags + pt)) == 0u) {
         }
         if (f == 2u) atomicMin(&s_stop, t);
       }
       __syncthreads();
       const int stop = s_stop;  // nearest P (kDlbThreads: none in the window)
-      // slot (last - t) holds predecessor base - t: time order ascending
-      const int slot = last - t;
-      if (t <= stop && pt >= 0) {
-        const S* src = f == 2u ? pincl : pagg;
-        for (int c = 0; c < Ops::kSize; ++c)
-          sm[c * kDlbSlots + slot] = __ldcg(src + (size_t)c * ntiles + pt);
+      if (stop < kDlbThreads) {
+        lo = base - stop;
+        break;
+      }
+      base -= kDlbThreads;  // tile 0 always carries P: the loop ends
+    }
+    // 5b. the exclusive prefix = incl(lo) (x) agg(lo+1) (x) ... (x) agg(tile-1):
+    // thread t folds the contiguous block [lo + t k, lo + (t+1) k) in time
+    // order into slot t, then an ordered 7-level tree over the slots -- k - 1
+    // + 7 combine latencies for any distance (a window-by-window reduction
+    // costs 7 per 128 predecessors)
+    {
+      const long long m = tile - lo;
+      const long long kb = (m + kDlbThreads - 1) / kDlbThreads;
+      const long long b0 = lo + t * kb;
+      const long long b1 = b0 + kb < tile ? b0 + kb : tile;
+      if (b0 < b1) {
+        ops.assign(sb, t, b0 == lo ? ib : ab, b0 * kDlbStride);
+        for (long long p = b0 + 1; p < b1; ++p) lcomb(sb, t, sb, t, ab, p * kDlbStride);
       } else {
-        ops.identity(sb, slot);
+        ops.identity(sb, t);
       }
       __syncthreads();
-      // ordered tree reduction of the window into slot 0
 #pragma unroll 1
       for (int d = 0; d < kDlbLevels; ++d) {
         const int s = 1 << d;
         if ((t & (2 * s - 1)) == 0) lcomb(sb, t, sb, t, sb, t + s);
         __syncthreads();
       }
-      if (t == 0) {
-        if (!have)
-          ops.assign(sb, kExcl, sb, 0);
-        else
-          lcomb(sb, kExcl, sb, 0, sb, kExcl);  // window is earlier: on the left
-      }
-      have = true;
+      if (t == 0) ops.assign(sb, kExcl, sb, 0);
       __syncthreads();
-      if (stop < kDlbThreads || base - kDlbThreads < 0) break;
-      base -= kDlbThreads;
     }
     dlb_stamp(trace, tile, 3);
     // 6. publish the inclusive prefix of the tile
     if (t == 0) {
       lcomb(sb, kTmp, sb, kExcl, sb, kTmp);
-      ops.assign(ib, tile, sb, kTmp);
+      ops.assign(ib, tile * kDlbStride, sb, kTmp);
       __threadfence();
       st_release(flags + tile, 2u);
     }

@@ -4,7 +4,7 @@ import sys
 
 import numpy as np
 
-raw = open(sys.argv[1], "rb").read()
+raw = open(sys.argv[1], "rb").read()  # usage: dlb_trace.py <PSK_DLB_TRACE file>
 off = 0
 while off < len(raw):
     nt, per, ks, n = np.frombuffer(raw, dtype=np.int64, count=4, offset=off)
