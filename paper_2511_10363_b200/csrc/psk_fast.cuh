@@ -453,12 +453,13 @@ struct FilterStage {
   }
 };
 
-// Double-buffered TMA walk over this thread's chunk c = steps [k0, k1).
-// body(k, stage) sees step k's inputs; step k+1's are in flight.  The walk
-// is CTA-uniform (every thread of the CTA must call it: block barriers), of
-// length min(L, T - first step of the CTA).  `nfull` = number of complete
+// Multi-buffered TMA walk over this thread's chunk c = steps [k0, k1)
+// (NS stages: step k's inputs are consumed while the next NS - 1 steps are in
+// flight; dynamic shared memory FilterTma::smem_n(NS)).  body(k, stage) sees step k's inputs.  The
+// walk is CTA-uniform (every thread of the CTA must call it: block barriers),
+// of length min(L, T - first step of the CTA).  `nfull` = number of complete
 // chunks (the extent of the tensor maps).
-template <typename S, int NX, int NY, class Body>
+template <typename S, int NX, int NY, int NS = 2, class Body>
 __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const StageMaps& maps,
                                             const ModelView<S>& m, long long L, long long nfull,
                                             long long k0, long long k1, Body&& body) {
@@ -466,7 +467,7 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
   using St = FilterStage<S, NX, NY>;
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * In::stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NS * In::stage);
   const int t = threadIdx.x;
   const long long cta0 = (long long)blockIdx.x * kStageNT;  // first chunk of the CTA
   const bool tma = cta0 < nfull;                            // CTA-uniform
@@ -489,26 +490,32 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
                     (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
     mbar_init_fence();
-    issue(0, 0);
+    for (int i = 0; i < NS - 1 && i < jn; ++i) issue(i, i);
   }
   __syncthreads();
+  int s = 0;           // stage of position j
+  unsigned phase = 0;  // its mbarrier phase
   for (long long j = 0; j < jn; ++j) {
-    const int s = (int)(j & 1);
-    if (tma && t == 0 && j + 1 < jn) issue(s ^ 1, j + 1);
-    if (tma) mbar_wait(&bars[s], (unsigned)((j >> 1) & 1));
+    // refill the stage consumed at j - 1 (all threads passed the barrier)
+    if (tma && t == 0 && j + NS - 1 < jn) issue(s == 0 ? NS - 1 : s - 1, j + NS - 1);
+    if (tma) mbar_wait(&bars[s], phase);
     if (k0 + j < k1) body(k0 + j, St{sm + s * In::stage, t, direct, &m, k0 + j, unstaged, g2, g4, (int)j});
     __syncthreads();  // stage s is refilled by the next iteration's issue
+    if (++s == NS) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
 }
 
-// The same double-buffered TMA walk, backwards: positions j = jn-1 .. 0 of
+// The same multi-buffered TMA walk, backwards: positions j = jn-1 .. 0 of
 // the chunk (body(k0 + j, stage) for the thread's positions inside [k0, k1);
 // `valid` positions are those < m.t, the others see no data).  `jn` is the
 // CTA-uniform walk length chosen by the caller.
-template <typename S, int NX, int NY, class Body>
+template <typename S, int NX, int NY, int NS = 2, class Body>
 __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const StageMaps& maps,
                                                 const ModelView<S>& m, long long L,
                                                 long long nfull, long long jn, long long k0,
@@ -517,7 +524,7 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
   using St = FilterStage<S, NX, NY>;
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * In::stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NS * In::stage);
   const int t = threadIdx.x;
   const long long cta0 = (long long)blockIdx.x * kStageNT;
   const bool tma = cta0 < nfull;
@@ -529,7 +536,8 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
     g2 |= (maps.grp[f] == 2 ? 1u : 0u) << f;
     g4 |= (maps.grp[f] == 4 ? 1u : 0u) << f;
   }
-  // positions >= the m-length of the CTA's first chunk carry no data
+  // positions >= the m-length of the CTA's first chunk carry no data; the
+  // i-th fetch is position jd - 1 - i
   const long long jd = min(jn, max(0LL, m.t - cta0 * L));
   auto issue = [&](int s, long long j) {
     fence_proxy_async();
@@ -541,24 +549,27 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
                     (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
     mbar_init_fence();
-    if (jd > 0) issue(0, jd - 1);
+    for (int i = 0; i < NS - 1 && i < jd; ++i) issue(i, jd - 1 - i);
   }
   __syncthreads();
-  long long it = 0;  // fetches consumed so far
+  int s = 0;  // stage of the next fetch consumed
+  unsigned phase = 0;
   for (long long j = jn - 1; j >= 0; --j) {
     const bool data = j < jd;
-    const int s = (int)(it & 1);
     if (data) {
-      if (tma && t == 0 && j >= 1) issue(s ^ 1, j - 1);
-      if (tma) mbar_wait(&bars[s], (unsigned)((it >> 1) & 1));
+      if (tma && t == 0 && j - (NS - 1) >= 0) issue(s == 0 ? NS - 1 : s - 1, j - (NS - 1));
+      if (tma) mbar_wait(&bars[s], phase);
     }
     const long long k = k0 + j;
     if (k < k1) body(k, k < m.t, St{sm + s * In::stage, t, direct, &m, k, unstaged, g2, g4, (int)j});
     __syncthreads();
-    if (data) ++it;
+    if (data && ++s == NS) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
 }
 
@@ -725,7 +736,8 @@ __global__ void __launch_bounds__(kStageNT, 2)
   Mat<S, NX, NX> P = zeros<S, NX, NX>();
   if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
   SElem<S, NX> sa = se_identity<S, NX>();
-  staged_walk<S, NX, NY>(fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
+  staged_walk<S, NX, NY, FilterTma<S, NX, NY>::finish_stages>(
+      fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
     const Mat<S, NX, NX> F = in.F();
     const Vec<S, NX> xp = mul_add(F, x, in.u());
     const Mat<S, NX, NX> fp = mul(F, P);
@@ -807,8 +819,9 @@ __global__ void __launch_bounds__(kSmoothNT)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       ((reinterpret_cast<uintptr_t>(ssm_raw) + 1023) & ~uintptr_t(1023)) + (size_t)w * Tm::warp);
-  unsigned char* egl_st = sm;                                   // 2 x egl_stage
-  unsigned char* mean_st = sm + 2 * Tm::egl_stage;              // 2 x mean_stage
+  constexpr int ENS = Tm::egl_nstage;
+  unsigned char* egl_st = sm;                                   // ENS x egl_stage
+  unsigned char* mean_st = sm + ENS * Tm::egl_stage;            // 2 x mean_stage
   unsigned char* cov_st = mean_st + 2 * Tm::mean_stage;         // 2 x cov_stage
   uint64_t* bars = reinterpret_cast<uint64_t*>(cov_st + 2 * Tm::cov_stage);
   const long long cw0 = (long long)blockIdx.x * kSmoothNT + w * 32;  // first chunk of the warp
@@ -846,18 +859,21 @@ __global__ void __launch_bounds__(kSmoothNT)
     mbar_expect_tx(&bars[st], (unsigned)Tm::egl_box);
     tma_load_2d(egl_st + st * Tm::egl_stage, &maps.egl, (int)cw0, (int)(j * ES), &bars[st]);
   };
+  // the i-th fetch is position jn - 1 - i, into stage i mod ENS
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int i = 0; i < ENS; ++i) mbar_init(&bars[i], 1);
     mbar_init_fence();
-    issue((int)((jn - 1) & 1), jn - 1);
+    for (int i = 0; i < ENS - 1 && i < jn; ++i) issue(i, jn - 1 - i);
   }
   __syncwarp();
+  int es = 0;  // element stage of position j
+  unsigned ephase = 0;
   for (long long j = jn - 1; j >= 0; --j) {
-    const int st = (int)(j & 1);
-    if (lane == 0 && j > 0) issue(st ^ 1, j - 1);
-    mbar_wait(&bars[st], (unsigned)(((jn - 1 - j) >> 1) & 1));
-    const S* el = reinterpret_cast<const S*>(egl_st + st * Tm::egl_stage);
+    const int st = (int)(j & 1);  // output stage
+    if (lane == 0 && j - (ENS - 1) >= 0) issue(es == 0 ? ENS - 1 : es - 1, j - (ENS - 1));
+    mbar_wait(&bars[es], ephase);
+    const S* el = reinterpret_cast<const S*>(egl_st + es * Tm::egl_stage);
     const bool act = live && k0 + j < k1;
     if (act) {
       SElem<S, NX> ei;
@@ -900,7 +916,11 @@ __global__ void __launch_bounds__(kSmoothNT)
       }
     }
     if (act && direct_out) store_state(mean, cov, k0 + j, gs, Ls);
-    __syncwarp();  // stage st of the elements is refilled next iteration
+    __syncwarp();  // stage es of the elements is refilled next iteration
+    if (++es == ENS) {
+      es = 0;
+      ephase ^= 1u;
+    }
   }
   if (lane == 0) bulk_wait<0>();
 }

@@ -174,7 +174,7 @@ int group_mult(const ModelView<S>& m) {
 template <typename S, int NX, int NY>
 long long auto_chunk(long long T, int waves, int mult = 1) {
   const int per_sm = kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT,
-                                  FilterTma<S, NX, NY>::smem);
+                                  FilterTma<S, NX, NY>::smem_n(FilterTma<S, NX, NY>::finish_stages));
   const long long wave = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kStageNT;
   const long long L = (T + wave * (waves > 0 ? waves : 1) - 1) / (wave * (waves > 0 ? waves : 1));
   // ... but at least 64 steps per chunk unless that leaves less than one
@@ -260,8 +260,10 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
     }
   };
   const int gs = blocks_for(nch, kStageNT);
-  // TMA stage of the per-step inputs (psk_stage.cuh): two stages of the CTA
+  // TMA stages of the per-step inputs (psk_stage.cuh): two for the reduce
+  // and backward passes, FilterTma::finish_stages for the filter finish
   const int stage_bytes = FilterTma<S, NX, NY>::smem;
+  const int finish_bytes = FilterTma<S, NX, NY>::smem_n(FilterTma<S, NX, NY>::finish_stages);
   const long long nfull = m.t / Lc;  // complete chunks (extent of the tensor maps)
   StageMaps maps;
   if (phase == 0 || phase == 1) {
@@ -283,14 +285,14 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       break;
     case 1:  // filter finish; for PRTS also folds the smoother chunk elements
       if (a.method == 1) {
-        kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT, stage_bytes);
-        k_filter_finish<S, NX, NY, true><<<gs, kStageNT, stage_bytes, L.stream>>>(
+        kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT, finish_bytes);
+        k_filter_finish<S, NX, NY, true><<<gs, kStageNT, finish_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, sc.sagg, npad, sc.egl,
             sc.ecap, L.err);
         L.count("filter_finish_smoother_reduce");
       } else {
-        kernel_setup(k_filter_finish<S, NX, NY, false>, kStageNT, stage_bytes);
-        k_filter_finish<S, NX, NY, false><<<gs, kStageNT, stage_bytes, L.stream>>>(
+        kernel_setup(k_filter_finish<S, NX, NY, false>, kStageNT, finish_bytes);
+        k_filter_finish<S, NX, NY, false><<<gs, kStageNT, finish_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad,
             a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
         L.count("filter_finish");

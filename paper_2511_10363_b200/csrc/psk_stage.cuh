@@ -155,9 +155,16 @@ struct FilterTma {
     return f == 0 ? F::row : f == 1 ? u::row : f == 2 ? Q::row : f == 3 ? H::row
          : f == 4 ? d::row : f == 5 ? R::row : y::row;
   }
-  // dynamic shared memory of a double-buffered walk (+ alignment slack and
-  // the two mbarriers)
-  static constexpr int smem = 2 * stage + 1024 + 64;
+  // dynamic shared memory of a walk with `ns` stages (steps in flight + 1),
+  // + alignment slack and the mbarriers
+  __host__ __device__ static constexpr int smem_n(int ns) { return ns * stage + 1024 + 64; }
+  static constexpr int smem = smem_n(2);
+  // stages of the filter finish: an FP32 step is cheaper and its stage half
+  // as large, so two stages leave the finish waiting on TMA latency; three
+  // (28 KB each at nx = 4) still fit its 2 CTAs per SM (register-bound).
+  // The reduce keeps two (3 CTAs/SM in FP32: measured faster than 2 x 3
+  // stages; 4 stages fit only 1 CTA/SM, 2x slower).  FP64: two 53 KB stages.
+  static constexpr int finish_stages = sizeof(S) == 4 ? 3 : 2;
 };
 
 // this thread's row of a staged field <- a row-major R x C matrix (the
@@ -209,8 +216,12 @@ struct SmoothTma {
   static constexpr int mean_stage = (Mean::row * 32 + 1023) / 1024 * 1024;
   using Cov = TField<0, NX * NX * (int)sizeof(S)>;
   static constexpr int cov_stage = (Cov::row * 32 + 1023) / 1024 * 1024;
-  // one warp: 2 egl stages, 2 mean stages, 2 cov stages, 2 mbarriers
-  static constexpr int warp = 2 * (egl_stage + mean_stage + cov_stage) + 1024;
+  // element stages of the per-warp pipeline (FP32 boxes are half as large
+  // and the step is cheaper: more of them in flight, as in FilterTma)
+  static constexpr int egl_nstage = sizeof(S) == 4 ? 4 : 2;
+  // one warp: egl_nstage egl stages, 2 mean stages, 2 cov stages, mbarriers
+  static constexpr int warp =
+      egl_nstage * egl_stage + 2 * (mean_stage + cov_stage) + 1024;
 };
 
 }  // namespace psk
