@@ -216,9 +216,10 @@ struct SmoothTma {
   static constexpr int mean_stage = (Mean::row * 32 + 1023) / 1024 * 1024;
   using Cov = TField<0, NX * NX * (int)sizeof(S)>;
   static constexpr int cov_stage = (Cov::row * 32 + 1023) / 1024 * 1024;
-  // element stages of the per-warp pipeline (FP32 boxes are half as large
-  // and the step is cheaper: more of them in flight, as in FilterTma)
-  static constexpr int egl_nstage = sizeof(S) == 4 ? 4 : 2;
+  // element stages of the per-warp pipeline: four (3 boxes in flight per
+  // warp; FP64 2 CTAs/SM, FP32 4) -- measured against 2 and 3 stages:
+  // FP64 1.165 / 1.133 / 1.116 ms, FP32 0.671 (2) / 0.629 ms (4) at 2^24
+  static constexpr int egl_nstage = 4;
   // one warp: egl_nstage egl stages, 2 mean stages, 2 cov stages, mbarriers
   static constexpr int warp =
       egl_nstage * egl_stage + 2 * (mean_stage + cov_stage) + 1024;
