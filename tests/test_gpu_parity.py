@@ -416,3 +416,35 @@ def test_batch_errors(psk, gpu, port):
     got = psk.prts_run_batch([m], [ys], spec, be)  # the context is usable after it
     assert got[0].mean.shape == (300, 4)
     assert psk.prts_run_batch([], [], spec, be) == []
+
+
+def test_async_two_contexts_host_buffers(psk, gpu, port):
+    """The e2e pattern of bench.py: two contexts in async mode take alternate
+    series from pinned HOST inputs into pinned HOST outputs; after each
+    context's sync its outputs equal the synchronous call's, bitwise."""
+    import torch
+    m, ys = gen(port, 77, 4, 2, 20000)
+    pin = lambda a: torch.as_tensor(np.asarray(a)).pin_memory()  # noqa: E731
+    mh = psk.Lgssm(f=pin(m.f), u=pin(m.u), q=pin(m.q), h=pin(m.h), d=pin(m.d), r=pin(m.r),
+                   prior_mean=pin(m.prior_mean), prior_cov=pin(m.prior_cov), t=m.t)
+    yh = pin(ys)
+    spec = psk.ScanSpec(psk.ScanAlg(6))
+    want = psk.prts_run(mh, yh, spec, psk.CudaBackend(gpu))
+    bes = [psk.CudaBackend(gpu), psk.CudaBackend(gpu)]
+    outs = [psk.GaussianStats(torch.empty((m.t, 4), dtype=torch.float64).pin_memory(),
+                              torch.empty((m.t, 4, 4), dtype=torch.float64).pin_memory())
+            for _ in range(2)]
+    for b in bes:
+        b.set_option("async", 1)
+    for i in range(6):
+        j = i % 2
+        if i >= 2:
+            bes[j].sync()
+            assert torch.equal(outs[j].mean, want.mean) and torch.equal(outs[j].cov, want.cov)
+            outs[j].mean.zero_()
+            outs[j].cov.zero_()
+        psk.prts_run(mh, yh, spec, bes[j], out=outs[j])
+    for j in range(2):
+        bes[j].sync()
+        assert torch.equal(outs[j].mean, want.mean) and torch.equal(outs[j].cov, want.cov)
+        bes[j].set_option("async", 0)
