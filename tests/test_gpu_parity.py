@@ -448,3 +448,34 @@ def test_async_two_contexts_host_buffers(psk, gpu, port):
         bes[j].sync()
         assert torch.equal(outs[j].mean, want.mean) and torch.equal(outs[j].cov, want.cov)
         bes[j].set_option("async", 0)
+
+
+def test_contexts_from_concurrent_host_threads(psk, gpu, port):
+    """Distinct contexts may be driven from different host threads at once
+    (psk.h threading contract; ctypes releases the GIL during the calls)."""
+    import threading
+    m, ys = gen(port, 81, 4, 2, 30000)
+    m2, ys2 = gen(port, 83, 3, 2, 7000)
+    spec = psk.ScanSpec(psk.ScanAlg(6))
+    want = [psk.prts_run(m, ys, spec, psk.CudaBackend(gpu)),
+            psk.pkf_run(m2, ys2, psk.ScanSpec(psk.ScanAlg(3)), psk.CudaBackend(gpu))]
+    errs = []
+
+    def work(i):
+        try:
+            be = psk.CudaBackend(gpu)
+            for _ in range(5):
+                got = (psk.prts_run(m, ys, spec, be) if i == 0 else
+                       psk.pkf_run(m2, ys2, psk.ScanSpec(psk.ScanAlg(3)), be))
+                if not (np.array_equal(got.mean, want[i].mean) and
+                        np.array_equal(got.cov, want[i].cov)):
+                    errs.append(f"thread {i}: result differs")
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"thread {i}: {e!r}")
+
+    th = [threading.Thread(target=work, args=(i,)) for i in (0, 1, 0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
