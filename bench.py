@@ -414,7 +414,7 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
         psk.prts_run(m, ys, spec, bes[j], out=outs[j])
     for b in bes:
         b.sync()
-    psteps = max(4, min(args.steps, 8))
+    psteps = max(4, min(args.steps, 16))  # fill / drain of the 2-deep pipeline amortised
     t0 = time.perf_counter()
     for i in range(psteps):
         j = i % 2
