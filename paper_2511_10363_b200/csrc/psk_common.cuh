@@ -38,6 +38,32 @@ struct ModelView {
 // p[c * cap + i] (coalesced across consecutive slots).  `rev` implements the
 // reference's Reversed<E> adapter (scan.hpp:149-177): logical slot i lives at
 // physical cap-1-i ... of the logical size `n`.
+// Storage slot of chunk c in a chunk-element buffer (SoA, one slot per
+// chunk).  per = 0: chunk order.  per >= 1 (buffers scanned by the decoupled
+// look-back, psk_dlb.cuh): slots follow the SCAN order (reversed for reverse
+// scans) and, inside each tile of kOrderNT * per elements, element
+// r = t per + j of the tile sits at j kOrderNT + t -- the per consecutive
+// elements of look-back thread t are then coalesced across the threads.
+constexpr int kOrderNT = 128;  // == kDlbThreads
+struct ChunkOrder {
+  long long n;  // chunks
+  int per;
+  int rev;
+  __host__ __device__ __forceinline__ long long at(long long c) const {
+    if (per == 0) return c;
+    const long long g = rev ? n - 1 - c : c;
+    const long long tile = (long long)kOrderNT * per;
+    const long long b = g / tile * tile, r = g - b;
+    return b + (r % per) * kOrderNT + r / per;
+  }
+  // slots a buffer in this order needs
+  __host__ __device__ long long cap() const {
+    if (per == 0) return n;
+    const long long tile = (long long)kOrderNT * per;
+    return (n + tile - 1) / tile * tile;
+  }
+};
+
 template <typename S>
 struct ElemBuf {
   S* p;

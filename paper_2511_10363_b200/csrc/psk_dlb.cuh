@@ -39,6 +39,7 @@
 namespace psk {
 
 constexpr int kDlbThreads = 128;
+static_assert(kDlbThreads == kOrderNT, "ChunkOrder tiles are look-back tiles");
 constexpr int kDlbLevels = 7;  // log2(kDlbThreads)
 static_assert((1 << kDlbLevels) == kDlbThreads, "CTA must be 2^kDlbLevels threads");
 constexpr int kDlbSlots = kDlbThreads + 2;  // + exclusive tile prefix + scratch
@@ -96,13 +97,13 @@ inline size_t dlb_state_bytes(long long n) {
 
 template <class Ops>
 __global__ void __launch_bounds__(kDlbThreads)
-    k_dlb(Ops ops, typename Ops::S* buf, long long n, int rev, char* state,
-          long long ntiles, int per, unsigned long long* trace) {
+    k_dlb(Ops ops, typename Ops::S* buf, long long n, long long cap, int rev, int perm,
+          char* state, long long ntiles, int per, unsigned long long* trace) {
   using S = typename Ops::S;
   extern __shared__ __align__(16) unsigned char dlb_smem[];
   S* sm = reinterpret_cast<S*>(dlb_smem);
   const ElemBuf<S> sb{sm, kDlbSlots, kDlbSlots, 0};
-  const ElemBuf<S> gb{buf, n, n, 0};
+  const ElemBuf<S> gb{buf, cap, n, 0};
   unsigned* ticket = reinterpret_cast<unsigned*>(state);
   unsigned* flags = reinterpret_cast<unsigned*>(state + 256);
   static_assert(Ops::kSize <= kDlbStride, "element wider than the payload stride");
@@ -130,7 +131,10 @@ __global__ void __launch_bounds__(kDlbThreads)
     else
       ops.combine(d, di, r, ri, l, li);
   };
-  auto phys = [&](long long g) { return rev ? n - 1 - g : g; };
+  // slot of scan element g: the ChunkOrder of the buffer (perm: the tile
+  // transpose, already in scan order) or the reference's Reversed map
+  const ChunkOrder ord{n, per, 0};
+  auto phys = [&](long long g) { return perm ? ord.at(g) : (rev ? n - 1 - g : g); };
 
   // 2. serial fold of this thread's K consecutive elements into slot t
   const long long g0 = (tile * kDlbThreads + t) * per;
@@ -278,14 +282,26 @@ __global__ void __launch_bounds__(kDlbThreads)
   dlb_stamp(trace, tile, 5);
 }
 
+// Elements per thread of a k_dlb<Ops> scan of n elements on this device
+// (also the `per` of the ChunkOrder its buffer is stored in).
 template <class Ops>
-void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf,
-              long long n, int rev, typename Ops::S* /*unused*/, void* state) {
+int dlb_per(long long n) {
+  using S = typename Ops::S;
+  const size_t smem = sizeof(S) * (size_t)Ops::kSize * kDlbSlots;
+  const int per_sm = kernel_setup(k_dlb<Ops>, kDlbThreads, (int)smem);
+  return dlb_per_thread(n, (long long)device_sms() * per_sm);
+}
+
+// `cap`: component stride of buf; `perm`: buf is stored in ChunkOrder{n,
+// dlb_per<Ops>(n), rev} (scan-order slots, tile-transposed), else in chunk
+// order read through the Reversed map when rev.
+template <class Ops>
+void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf, long long n,
+              long long cap, int rev, int perm, void* state) {
   using S = typename Ops::S;
   if (n <= 0) return;
   const size_t smem = sizeof(S) * (size_t)Ops::kSize * kDlbSlots;
-  const int per_sm = kernel_setup(k_dlb<Ops>, kDlbThreads, (int)smem);
-  const int per = dlb_per_thread(n, (long long)device_sms() * per_sm);
+  const int per = dlb_per<Ops>(n);
   const long long ntiles = dlb_tiles(n, per);
   cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
   static unsigned long long* trace = nullptr;  // PSK_DLB_TRACE: stamps of the last scan
@@ -295,7 +311,7 @@ void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf,
     trace_tiles = ntiles;
   }
   k_dlb<Ops><<<(unsigned)ntiles, kDlbThreads, smem, L.stream>>>(
-      ops, buf, n, rev, reinterpret_cast<char*>(state), ntiles, per,
+      ops, buf, n, cap, rev, perm, reinterpret_cast<char*>(state), ntiles, per,
       trace != nullptr && ntiles <= 65536 ? trace : nullptr);
   if (trace != nullptr && std::getenv("PSK_DLB_TRACE") != nullptr) {
     std::vector<unsigned long long> h((size_t)trace_tiles * 8);

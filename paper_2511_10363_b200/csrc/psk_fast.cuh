@@ -617,7 +617,8 @@ __device__ __forceinline__ SElem<S, NX> terminal_elem(const Vec<S, NX>& x,
 template <typename S, int NX, int NY>
 __global__ void __launch_bounds__(kStageNT, sizeof(S) == 8 ? 2 : 3)
     k_filter_reduce(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
-                    long long nchunks, long long nfull, S* agg, long long cap, unsigned* err) {
+                    long long nchunks, long long nfull, S* agg, long long cap, ChunkOrder ord,
+                    unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = c < nchunks;  // idle threads stay for the block barriers
@@ -646,7 +647,7 @@ __global__ void __launch_bounds__(kStageNT, sizeof(S) == 8 ? 2 : 3)
     a.C = mul_nt_sym_add(fc, F, in.Q());
     cond_update(a, in.meas(), e);
   });
-  if (live) fe_store(agg, cap, c, a);
+  if (live) fe_store(agg, cap, ord.at(c), a);
   if (e) atomicOr(err, e);
 }
 
@@ -657,8 +658,9 @@ __global__ void __launch_bounds__(kStageNT, sizeof(S) == 8 ? 2 : 3)
 template <typename S, int NX>
 __device__ __forceinline__ void filter_incoming(const ModelView<S>& m, long long c,
                                                 const S* pre, long long pre_cap,
-                                                const S* carry, Vec<S, NX>& x,
-                                                Mat<S, NX, NX>& P, unsigned& e) {
+                                                ChunkOrder pord, const S* carry,
+                                                Vec<S, NX>& x, Mat<S, NX, NX>& P,
+                                                unsigned& e) {
   if (c == 0) {
     if (m.prior_first) {
       x = load<S, NX, 1>(m.m0);
@@ -668,12 +670,13 @@ __device__ __forceinline__ void filter_incoming(const ModelView<S>& m, long long
       P = load<S, NX, NX>(carry + NX);
     }
   } else if (carry == nullptr) {
-    x = load_soa<S, NX, 1>(pre + FLayout<NX>::b * pre_cap + (c - 1), pre_cap);
-    P = load_soa<S, NX, NX>(pre + FLayout<NX>::C * pre_cap + (c - 1), pre_cap);
+    const long long q = pord.at(c - 1);
+    x = load_soa<S, NX, 1>(pre + FLayout<NX>::b * pre_cap + q, pre_cap);
+    P = load_soa<S, NX, NX>(pre + FLayout<NX>::C * pre_cap + q, pre_cap);
   } else {
     x = load<S, NX, 1>(carry);
     P = load<S, NX, NX>(carry + NX);
-    filter_apply(x, P, fe_load<S, NX>(pre, pre_cap, c - 1), e);
+    filter_apply(x, P, fe_load<S, NX>(pre, pre_cap, pord.at(c - 1)), e);
   }
 }
 
@@ -722,8 +725,8 @@ template <typename S, int NX, int NY, bool SMOOTH>
 __global__ void __launch_bounds__(kStageNT, 2)
     k_filter_finish(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
                     long long nchunks, long long nfull, const S* pre, long long pre_cap,
-                    const S* carry, S* mean, S* cov, S* sagg, long long scap, S* egl,
-                    long long ecap, unsigned* err) {
+                    ChunkOrder pord, const S* carry, S* mean, S* cov, S* sagg,
+                    long long scap, ChunkOrder sord, S* egl, long long ecap, unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = c < nchunks;  // idle threads stay for the block barriers
@@ -734,7 +737,7 @@ __global__ void __launch_bounds__(kStageNT, 2)
   using St = FilterStage<S, NX, NY>;
   Vec<S, NX> x = zeros<S, NX, 1>();
   Mat<S, NX, NX> P = zeros<S, NX, NX>();
-  if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, carry, x, P, e);
+  if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, pord, carry, x, P, e);
   SElem<S, NX> sa = se_identity<S, NX>();
   staged_walk<S, NX, NY, FilterTma<S, NX, NY>::finish_stages>(
       fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
@@ -782,7 +785,7 @@ __global__ void __launch_bounds__(kStageNT, 2)
                            load<S, NX, 1>(m.U(k1)), e);
       egl_store(egl + (k1 - 1 - k0) * ES * ecap + c, ecap, ek);
       sa = smoother_combine(sa, ek);
-      se_store(sagg, scap, c, sa);
+      se_store(sagg, scap, sord.at(c), sa);
     }
   }
   if (e) atomicOr(err, e);
@@ -811,7 +814,7 @@ constexpr int kSmoothNT = 64;  // 2 warps per CTA
 template <typename S, int NX>
 __global__ void __launch_bounds__(kSmoothNT)
     k_smoother_finish(long long t, long long L, long long nchunks, long long nfull,
-                      const S* suf, long long suf_cap, const S* carry,
+                      const S* suf, long long suf_cap, ChunkOrder sord, const S* carry,
                       const __grid_constant__ SmoothMaps maps, long long ecap, S* mean, S* cov) {
   using Tm = SmoothTma<S, NX>;
   constexpr int ES = Tm::ES;
@@ -837,11 +840,11 @@ __global__ void __launch_bounds__(kSmoothNT)
   Vec<S, NX> gs = zeros<S, NX, 1>();
   Mat<S, NX, NX> Ls = zeros<S, NX, NX>();
   if (live && c + 1 < nchunks) {
-    gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + (c + 1), suf_cap);
-    Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + (c + 1), suf_cap);
+    const long long q = sord.at(c + 1);
+    gs = load_soa<S, NX, 1>(suf + SLayout<NX>::g * suf_cap + q, suf_cap);
+    Ls = load_soa<S, NX, NX>(suf + SLayout<NX>::L * suf_cap + q, suf_cap);
     if (carry != nullptr) {
-      const Mat<S, NX, NX> E =
-          load_soa<S, NX, NX>(suf + SLayout<NX>::E * suf_cap + (c + 1), suf_cap);
+      const Mat<S, NX, NX> E = load_soa<S, NX, NX>(suf + SLayout<NX>::E * suf_cap + q, suf_cap);
       const Vec<S, NX> cg = load<S, NX, 1>(carry);
       const Mat<S, NX, NX> cl = load<S, NX, NX>(carry + NX);
       gs = mul_add(E, cg, gs);
@@ -940,7 +943,7 @@ template <typename S, int NX, int NY>
 __global__ void __launch_bounds__(kStageNT, 2)
     k_bwd_finish(ModelView<S> ms, const __grid_constant__ StageMaps maps, long long T,
                  long long L, long long nchunks, long long nfull, const S* suf, long long suf_cap,
-                 const S* fst, long long fcap, S* mean, S* cov, unsigned* err) {
+                 ChunkOrder bord, const S* fst, long long fcap, S* mean, S* cov, unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   using St = FilterStage<S, NX, NY>;
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -953,8 +956,9 @@ __global__ void __launch_bounds__(kStageNT, 2)
   Vec<S, NX> eta = zeros<S, NX, 1>();
   Mat<S, NX, NX> J = zeros<S, NX, NX>();
   if (live && c + 1 < nchunks) {
-    eta = load_soa<S, NX, 1>(suf + FLayout<NX>::eta * suf_cap + (c + 1), suf_cap);
-    J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + (c + 1), suf_cap);
+    const long long q = bord.at(c + 1);
+    eta = load_soa<S, NX, 1>(suf + FLayout<NX>::eta * suf_cap + q, suf_cap);
+    J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + q, suf_cap);
   }
   staged_walk_rev<S, NX, NY>(fsm, maps, ms, L, nfull, jn, k0, k1,
                              [&](long long i, bool has, const St& in) {

@@ -89,10 +89,10 @@ template <class Ops>
 static void chunk_scan(ExactLaunch& L, const Ops& ops, const FastArgs& a,
                        typename Ops::S* buf, long long nchunks, long long npad,
                        int rev, typename Ops::S* aux1, typename Ops::S* aux2,
-                       const ScanPlan& plan, void* dlb_state) {
+                       const ScanPlan& plan, void* dlb_state, long long cap = 0) {
   using S = typename Ops::S;
-  if (a.alg == 6) {
-    dlb_scan<Ops>(L, ops, buf, nchunks, rev, aux1, dlb_state);
+  if (a.alg == 6) {  // buf in ChunkOrder{nchunks, dlb_per<Ops>, rev} (FastScratch)
+    dlb_scan<Ops>(L, ops, buf, nchunks, cap, rev, 1, dlb_state);
     return;
   }
   Bufs3<Ops> bufs;
@@ -195,6 +195,11 @@ long long auto_chunk(long long T, int waves, int mult = 1) {
 template <typename S>
 struct FastScratch {
   long long nchunks = 0, npad = 0, chunk = 1;
+  // component stride of agg / sagg (>= npad) and the slot orders of the
+  // filter (forward), smoother (reverse) and PTFS backward (reverse) chunk
+  // elements: tile-transposed scan order under the DLB, chunk order else
+  long long cap = 0;
+  ChunkOrder ford{0, 0, 0}, sord{0, 0, 0}, bord{0, 0, 0};
   ScanPlan plan;
   S *agg = nullptr, *aux1 = nullptr, *aux2 = nullptr;
   S* sagg = nullptr;        // smoother chunk elements (built by the filter finish)
@@ -218,8 +223,20 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
   }
   constexpr int FS = FLayout<NX>::size;
   const long long a1 = dlb ? 0 : sc.plan.cap1, a2 = dlb ? 0 : sc.plan.cap2;
-  sc.agg = (S*)alloc(sizeof(S) * FS * (sc.npad ? sc.npad : 1), actx);
-  sc.sagg = (S*)alloc(sizeof(S) * SLayout<NX>::size * (sc.npad ? sc.npad : 1), actx);
+  const long long nch = sc.nchunks;
+  if (dlb && nch > 0) {
+    const int pf = dlb_per<FastFilterOps<S, NX>>(nch);
+    const int ps = dlb_per<FastSmootherOps<S, NX>>(nch);
+    sc.ford = ChunkOrder{nch, pf, 0};
+    sc.sord = ChunkOrder{nch, ps, 1};
+    sc.bord = ChunkOrder{nch, pf, 1};
+    sc.cap = sc.ford.cap() > sc.sord.cap() ? sc.ford.cap() : sc.sord.cap();
+  } else {
+    sc.ford = sc.sord = sc.bord = ChunkOrder{nch, 0, 0};
+    sc.cap = sc.npad;
+  }
+  sc.agg = (S*)alloc(sizeof(S) * FS * (sc.cap ? sc.cap : 1), actx);
+  sc.sagg = (S*)alloc(sizeof(S) * SLayout<NX>::size * (sc.cap ? sc.cap : 1), actx);
   sc.sagg_valid = false;
   sc.egl = nullptr;
   sc.ecap = (sc.nchunks + 31) / 32 * 32;
@@ -274,12 +291,13 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
     case 0:
       kernel_setup(k_filter_reduce<S, NX, NY>, kStageNT, stage_bytes);
       k_filter_reduce<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
-          m, maps, Lc, nch, nfull, sc.agg, npad, L.err);
+          m, maps, Lc, nch, nfull, sc.agg, sc.cap, sc.ford, L.err);
       L.count("filter_reduce");
       fill(fops, sc.agg);
-      chunk_scan(L, fops, a, sc.agg, nch, npad, 0, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      chunk_scan(L, fops, a, sc.agg, nch, npad, 0, sc.aux1, sc.aux2, sc.plan, sc.dlb, sc.cap);
       if (elem_out) {
-        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, npad, nch - 1, FLayout<NX>::size, elem_out);
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, sc.cap, sc.ford.at(nch - 1),
+                                               FLayout<NX>::size, elem_out);
         L.count("extract_elem");
       }
       break;
@@ -287,14 +305,14 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       if (a.method == 1) {
         kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT, finish_bytes);
         k_filter_finish<S, NX, NY, true><<<gs, kStageNT, finish_bytes, L.stream>>>(
-            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, sc.sagg, npad, sc.egl,
-            sc.ecap, L.err);
+            m, maps, Lc, nch, nfull, sc.agg, sc.cap, sc.ford, carry, mean, cov, sc.sagg,
+            sc.cap, sc.sord, sc.egl, sc.ecap, L.err);
         L.count("filter_finish_smoother_reduce");
       } else {
         kernel_setup(k_filter_finish<S, NX, NY, false>, kStageNT, finish_bytes);
         k_filter_finish<S, NX, NY, false><<<gs, kStageNT, finish_bytes, L.stream>>>(
-            m, maps, Lc, nch, nfull, sc.agg, npad, carry, mean, cov, nullptr, npad,
-            a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
+            m, maps, Lc, nch, nfull, sc.agg, sc.cap, sc.ford, carry, mean, cov, nullptr,
+            sc.cap, sc.sord, a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
         L.count("filter_finish");
       }
       sc.sagg_valid = a.method == 1;
@@ -304,9 +322,10 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       // PRTS filter finish (phase 1)
       if (!sc.sagg_valid || sc.egl == nullptr) return 7;
       fill(sops, sc.sagg);
-      chunk_scan(L, sops, a, sc.sagg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      chunk_scan(L, sops, a, sc.sagg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb, sc.cap);
       if (elem_out) {
-        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.sagg, npad, 0, SLayout<NX>::size, elem_out);
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.sagg, sc.cap, sc.sord.at(0),
+                                               SLayout<NX>::size, elem_out);
         L.count("extract_elem");
       }
       break;
@@ -319,7 +338,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       const int smem = kSmoothNT / 32 * SmoothTma<S, NX>::warp + 1024;
       kernel_setup(k_smoother_finish<S, NX>, kSmoothNT, smem);
       k_smoother_finish<S, NX><<<blocks_for(nch, kSmoothNT), kSmoothNT, smem, L.stream>>>(
-          m.t, Lc, nch, nfull, sc.sagg, npad, carry, sm_maps, sc.ecap, mean, cov);
+          m.t, Lc, nch, nfull, sc.sagg, sc.cap, sc.sord, carry, sm_maps, sc.ecap, mean, cov);
     }
       L.count("smoother_finish");
       sc.sagg_valid = false;
@@ -336,16 +355,23 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       if (nch_s > 0) {
         kernel_setup(k_filter_reduce<S, NX, NY>, kStageNT, stage_bytes);
         k_filter_reduce<S, NX, NY><<<blocks_for(nch_s, kStageNT), kStageNT, stage_bytes,
-                                     L.stream>>>(ms, smaps, Lc, nch_s, ms.t / Lc, sc.agg, npad,
-                                                 L.err);
+                                     L.stream>>>(ms, smaps, Lc, nch_s, ms.t / Lc, sc.agg, sc.cap,
+                                                 sc.bord, L.err);
         L.count("bwd_reduce");
       }
-      if (npad > nch_s) {
+      if (sc.bord.per > 0) {  // DLB order: the (at most one) identity chunk's slot
+        for (long long c = nch_s; c < nch; ++c) {
+          const long long q = sc.bord.at(c);
+          k_fill_identity<<<1, kBlock, 0, L.stream>>>(fops, ElemBuf<S>{sc.agg, sc.cap, sc.cap, 0},
+                                                      q, q + 1);
+          L.count("fill_identity");
+        }
+      } else if (npad > nch_s) {
         k_fill_identity<<<blocks_for(npad - nch_s, kBlock), kBlock, 0, L.stream>>>(
             fops, ElemBuf<S>{sc.agg, npad, npad, 0}, nch_s, npad);
         L.count("fill_identity");
       }
-      chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb);
+      chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb, sc.cap);
       break;
     }
     case 5: {
@@ -355,7 +381,8 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       if (st) return st;
       kernel_setup(k_bwd_finish<S, NX, NY>, kStageNT, stage_bytes);
       k_bwd_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
-          ms, smaps, m.t, Lc, nch, ms.t / Lc, sc.agg, npad, sc.egl, sc.ecap, mean, cov, L.err);
+          ms, smaps, m.t, Lc, nch, ms.t / Lc, sc.agg, sc.cap, sc.bord, sc.egl, sc.ecap, mean,
+          cov, L.err);
       L.count("bwd_finish_tf_combine");
       break;
     }
@@ -415,8 +442,13 @@ static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, Exact
   if (st) return st;
   // the forward elements in sa.agg are dead after the forward finish
   cudaStreamWaitEvent(LA.stream, done_b, 0);
+  // both sides hold the backward elements in the same slot order
+  if (sa.cap != sb.cap || sa.bord.per != sb.bord.per) {
+    cudaEventDestroy(done_b);
+    return 7;
+  }
   cudaMemcpyPeerAsync(sa.agg, devA, sb.agg, devB,
-                      sizeof(S) * FLayout<NX>::size * (size_t)sa.npad, LA.stream);
+                      sizeof(S) * FLayout<NX>::size * (size_t)sa.cap, LA.stream);
   LA.count("ptfs_backward_elements_peer_copy");
   cudaEventDestroy(done_b);
   return fast_phase_t<S, NX, NY>(LA, mA, a, sa, 5, mean, cov, nullptr, nullptr);
