@@ -101,7 +101,7 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
 /* Named tuning options of the fast path:
  *   "chunk"     steps folded per thread, 0 = auto (same as psk_set_chunk)
  *   "waves"     auto chunk: the chunks fill this many waves of co-resident
- *               threads (default 4)
+ *               threads (default: 4 in FP64, 3 in FP32)
  *   "async"     1: psk_pkf / psk_prts / psk_ptfs return once their work is
  *               queued on the context's stream (outputs valid when the stream
  *               completes; errors are reported by psk_sync); default 0 =

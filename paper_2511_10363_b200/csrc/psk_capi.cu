@@ -38,7 +38,7 @@ struct psk_ctx {
   cudaStream_t stream = nullptr;
   int mode = PSK_MODE_FAST;
   long long chunk = 0;  // 0: auto (whole waves of chunks)
-  int waves = 4;        // waves of chunks for the auto chunk length
+  int waves = 0;        // waves of chunks for the auto chunk length (0: per precision)
   int shard_async = 0;  // shard phases 0-2 and folds return without a host sync
   int async = 0;        // drivers return once queued; psk_sync reports errors
   unsigned* d_err = nullptr;

@@ -106,7 +106,7 @@ struct FastArgs {
   int alg = 3;          // psk_alg
   unsigned long long sengupta_n = 1;
   long long chunk = 32;
-  int waves = 4;        // auto chunk (chunk = 0): whole waves of chunks
+  int waves = 0;        // auto chunk (chunk = 0): whole waves of chunks (0: default)
 };
 template <typename S>
 bool fast_supported(int nx, int ny);

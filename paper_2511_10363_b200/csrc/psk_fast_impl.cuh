@@ -176,7 +176,10 @@ long long auto_chunk(long long T, int waves, int mult = 1) {
   const int per_sm = kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT,
                                   FilterTma<S, NX, NY>::smem_n(FilterTma<S, NX, NY>::finish_stages));
   const long long wave = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kStageNT;
-  const long long L = (T + wave * (waves > 0 ? waves : 1) - 1) / (wave * (waves > 0 ? waves : 1));
+  // default: 4 waves in FP64, 3 in FP32 (tools/waves_sweep.py, profiles/r01_v13:
+  // FP32 2.67 ms at 3 waves against 2.73 at 4; FP64 flat within 1 % over 4..8)
+  const int w = waves > 0 ? waves : (sizeof(S) == 4 ? 3 : 4);
+  const long long L = (T + wave * w - 1) / (wave * w);
   // ... but at least 64 steps per chunk unless that leaves less than one
   // wave of chunks: short chunks make the per-chunk costs (incoming state,
   // chunk-end element) and the scan's element count dominate

@@ -600,7 +600,7 @@ long long wide_auto_chunk(long long T, int waves, int nm) {
   const int smem = step_smem<S>(nm);
   const int per_sm = kernel_setup(k_wide_finish<S, true>, 32 * kWarps, smem);
   const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
-                             kWarps * (waves > 0 ? waves : 1);
+                             kWarps * (waves > 0 ? waves : 4);  // 0: default 4
   const long long L = (T + resident - 1) / resident;
   return L < 1 ? 1 : L;
 }
