@@ -9,20 +9,27 @@ prts_run over the whole series.
 
   value  -- device-resident throughput: inputs already in HBM, outputs to HBM,
             CUDA events on the library's stream, max over ranks;
-  e2e    -- the same call through the public API with pinned HOST buffers:
-            H2D of all inputs and D2H of all outputs inside the timed region,
-            a stream of series on two async contexts so one series' input
-            copy overlaps the previous one's result copy (sync_value: one
-            synchronous call at a time).
+  e2e    -- the same PRTS with HOST buffers: at N=1 through the C-ABI with
+            pinned host inputs/outputs (H2D of all inputs and D2H of all
+            outputs inside the timed region; a stream of series on two async
+            contexts so one series' input copy overlaps the previous one's
+            result copy); at N>1 every rank copies its shard in from pinned
+            host memory, runs the sharded PRTS and copies its shard's result
+            out (max over ranks);
+  parity -- the output of the last timed step against the CPU oracle's
+            sequential kf_run + rts_run (oracle/psk_oracle.c, f64,
+            -ffp-contract=off) on the same inputs, over all T steps:
+            max |a-b|/(1+|b|) (bench.hpp:216-237), gate 1e-9 FP64 / 1e-4 FP32.
 
-With --gpus N > 1 (torchrun, one rank per GPU) the time axis is sharded: each
-rank filters / smooths its contiguous chunk, the shard aggregates are
-exchanged with an NCCL all_gather and folded (paper_2511_10363_b200/
-distributed.py); scaling is "strong" (T fixed).
+With --gpus N > 1 the time axis is sharded: each rank filters / smooths its
+contiguous chunk, the shard aggregates are exchanged with an NCCL all_gather
+and folded (paper_2511_10363_b200/distributed.py); scaling is "strong" (T
+fixed).  Run without torchrun, `--gpus N` re-launches itself under
+torch.distributed.run with N ranks (and fails if fewer GPUs are visible).
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libparascan_ref.so: prts_run with PoolBackend on all host
-threads) on a bounded sample of the same workload.
+threads) on a bounded sample of the same workload (T = 2^22 by default).
 """
 from __future__ import annotations
 
@@ -136,22 +143,39 @@ def kernel_bytes_per_step(nx: int, ny: int, s: int) -> dict:
             "smoother_finish": (egl + st) * s}
 
 
-def cpu_reference(T_sample: int, threads: int, runs: int, seed: int = 0) -> dict:
-    """The reference's own CPU path on the same workload (bounded sample)."""
-    from oracle.oracle import Oracle  # baseline leg only
+def cpu_reference(T_sample: int, threads: int, runs: int, seed: int = 0,
+                  per_alg_log2t: int = 20) -> dict:
+    """The reference's own CPU path on the same workload (bounded sample):
+    prts_run InplaceLaFi on PoolBackend(all host threads), the sequential
+    KF + RTS on one core, and every ScanAlg in f64 and f32 (convert_model)
+    at a smaller T (bench.hpp:259-323 runs the same matrix)."""
+    from oracle.oracle import ALGS, Oracle  # baseline leg only
     from paper_2511_10363_b200.synthetic import cv_model
 
     m, ys = cv_model(T_sample, seed=seed)
     h = Oracle("ref").time_handle(m, ys)
     h.time("prts", 3, 16, threads)  # warm-up
     ts = [h.time("prts", 3, 16, threads) for _ in range(runs)]
-    seq = [h.time("seq", 3, 16, 1) for _ in range(max(1, runs // 2))]
+    seq = [h.time("seq", 3, 16, 1) for _ in range(max(1, runs // 3))]
+    del h
+    tp = 1 << per_alg_log2t
+    mp, ysp = cv_model(tp, seed=seed)
+    per_alg = {}
+    for prec in ("f64", "f32"):
+        hp = Oracle("ref").time_handle(mp, ysp, f32=prec == "f32")
+        for name, alg in ALGS.items():
+            per_alg[f"{name}_{prec}"] = round(tp / hp.time("prts", alg, 16, threads), 1)
+        per_alg[f"sequential_kf_rts_1core_{prec}"] = round(tp / hp.time("seq", 3, 16, 1), 1)
+        del hp
     return {"value": T_sample * len(ts) / sum(ts), "unit": "time-steps/s",
             "cores": threads, "kind": "reference",
             "sample": f"prts_run InplaceLaFi PoolBackend({threads}) on the first "
                       f"T={T_sample} steps of the same damped-CV f64 workload, "
-                      f"{runs} runs",
-            "sequential_kf_rts_1core": T_sample * len(seq) / sum(seq)}
+                      f"median-free mean of {runs} runs after 1 warm-up",
+            "sequential_kf_rts_1core": T_sample * len(seq) / sum(seq),
+            "per_alg_prts_steps_per_s": per_alg,
+            "per_alg_sample": f"T={tp}, one run each, PoolBackend({threads}); "
+                              "sequential_* = kf_run + rts_run on 1 core"}
 
 
 def run_reference_arm(args) -> None:
@@ -159,7 +183,7 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    T_sample = 1 << args.ref_log2t
+    T_sample = 1 << args.ref_log2t  # default 2^22: the reference's large-T rate
     from oracle.oracle import Oracle
     from paper_2511_10363_b200.synthetic import cv_model
 
@@ -174,7 +198,9 @@ def run_reference_arm(args) -> None:
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(args, note=f"reference CPU sample T={T_sample}"),
+        "config": config(args, note=f"reference CPU sample T={T_sample} per step "
+                                   f"(the full T=2^{args.log2t} x {args.steps + args.warmup} "
+                                   f"runs would take too long on the host)"),
         "cpu_baseline": {"value": value, "unit": "time-steps/s", "cores": threads,
                          "kind": "reference",
                          "sample": f"prts_run InplaceLaFi PoolBackend({threads}), "
@@ -212,14 +238,106 @@ def main() -> None:
     ap.add_argument("--chunk", type=int, default=0, help="steps per chunk, 0 = auto (one wave)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--broadcast", action="store_true")
-    ap.add_argument("--ref-log2t", type=int, default=18)
+    ap.add_argument("--ref-log2t", type=int, default=22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     run_psk(args)
+
+
+def spawn(args) -> int:
+    """`--gpus N` outside torchrun: re-launch this script with N ranks (one
+    per GPU, NCCL), as the driver's torchrun launch would."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible",
+              file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class OracleRun(threading.Thread):
+    """The CPU oracle's sequential kf_run + rts_run over the whole series (f64,
+    time-invariant blocks read with stride 0), started early on rank 0 so it
+    runs while the GPU is timed (the timed region is device time)."""
+
+    def __init__(self, T: int, ys_np: np.ndarray):
+        super().__init__(daemon=True)
+        self.T, self.ys = T, ys_np
+        self.result = None
+        self.error = None
+        self.seconds = None
+
+    def run(self) -> None:
+        try:
+            from oracle.oracle import Oracle  # the checker (parity leg only)
+            from paper_2511_10363_b200.api import Lgssm
+            from paper_2511_10363_b200.synthetic import cv_matrices
+
+            F, Q, H, R, m0, P0 = cv_matrices()
+            m = Lgssm(f=F, u=np.zeros(4), q=Q, h=H, d=np.zeros(2), r=R, prior_mean=m0,
+                      prior_cov=P0, t=self.T)
+            t0 = time.perf_counter()
+            self.result = Oracle("port").rts_run(m, self.ys)
+            self.seconds = time.perf_counter() - t0
+        except Exception as e:  # noqa: BLE001
+            self.error = repr(e)
+
+
+def parity_check(orc, out, lo: int, hi: int, T: int, dev, pg, rank: int, f64: bool) -> dict:
+    """max |a-b|/(1+|b|) (bench.hpp:216-237) of the last timed output against
+    the oracle over every step; under N ranks rank 0's oracle result is
+    broadcast (NCCL) and every rank checks its own shard on its GPU."""
+    import torch
+
+    ok = torch.tensor([1.0 if rank != 0 or orc.result is not None else 0.0],
+                      device=dev, dtype=torch.float64)
+    if pg is not None:
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+    if ok.item() == 0.0:
+        return {"error": orc.error if rank == 0 else "oracle failed on rank 0"}
+    if rank == 0:
+        rm = torch.from_numpy(orc.result[0]).to(dev)
+        rc = torch.from_numpy(orc.result[1]).to(dev)
+    else:
+        rm = torch.empty((T, 4), dtype=torch.float64, device=dev)
+        rc = torch.empty((T, 4, 4), dtype=torch.float64, device=dev)
+    if pg is not None:
+        torch.distributed.broadcast(rm, 0)
+        torch.distributed.broadcast(rc, 0)
+
+    def err(got, ref):
+        g = got.to(torch.float64)
+        return ((g - ref).abs() / (1 + ref.abs())).max()
+
+    e = torch.stack([err(out.mean, rm[lo:hi]), err(out.cov, rc[lo:hi])]).max().reshape(1)
+    if pg is not None:
+        torch.distributed.all_reduce(e, op=torch.distributed.ReduceOp.MAX)
+    tol = 1e-9 if f64 else 1e-4
+    res = {"max_rel_err": float(e.item()), "tol": tol, "pass": bool(e.item() <= tol),
+           "steps_checked": T, "checked": "smoothed means and covariances of the last "
+           "timed step, every time step",
+           "oracle": "sequential kf_run + rts_run, oracle/psk_oracle.c (f64, "
+                     "-ffp-contract=off; pinned bitwise to the reference), same inputs"}
+    if rank == 0 and orc.seconds is not None:
+        res["oracle_seconds"] = round(orc.seconds, 1)
+    return res
 
 
 def run_psk(args) -> None:
@@ -232,6 +350,8 @@ def run_psk(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -248,6 +368,10 @@ def run_psk(args) -> None:
     # ---- synthetic inputs (same series on every rank; each rank keeps its shard)
     F, Q, H, R, m0, P0 = cv_matrices()
     ys_np = simulate_cv(T, seed=0)
+    orc = None
+    if not args.no_parity and rank == 0:
+        orc = OracleRun(T, ys_np)
+        orc.start()
     lo, hi = dist_psk.shard_range(T, rank, world)
     hi_in = min(hi + 1, T)  # one extra transition for the smoother boundary
 
@@ -289,16 +413,18 @@ def run_psk(args) -> None:
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     be.set_profile(True)
+    out = None
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            out = step()
             launches += be.last_launch_count()
         ev1.record(stream)
         torch.cuda.synchronize()
     be.sync()  # raises on any device error of the timed steps
     be.set_profile(False)
+    be.set_option("async", 0)
     for name, kms in be.last_profile():
         prof.setdefault(name, []).append(kms)
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -307,6 +433,16 @@ def run_psk(args) -> None:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     value = T / (ms * 1e-3)
+
+    # ---- parity of the timed output against the CPU oracle (all T steps)
+    parity = None
+    if not args.no_parity:
+        if orc is not None:
+            orc.join()
+        with torch.cuda.stream(stream):
+            parity = parity_check(orc, out, lo, hi, T, dev, pg, rank, f64)
+        torch.cuda.synchronize()
+    del out
 
     # ---- roofline of the dominant kernel (per-launch averages, this run)
     peaks = _peaks()
@@ -334,16 +470,20 @@ def run_psk(args) -> None:
         if k in bps:
             kernels[k]["GBps"] = round(bps[k] * steps_local / (kernels[k]["avg_ms"] * 1e-3) / 1e9, 1)
 
-    # ---- end to end through the public API with pinned host buffers
+    # ---- end to end with host buffers
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local)
+    if not args.no_e2e:
+        if world == 1:
+            e2e = run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local)
+        else:
+            e2e = run_e2e_sharded(args, psk, dist_psk, model, ys, spec, be, stream, rank,
+                                  world, lo, hi, T, pg, dev)
 
     # ---- CPU baseline (reference CPU path, rank 0, N=1 only)
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         try:
-            cpu = cpu_reference(1 << args.ref_log2t, os.cpu_count() or 1, runs=8)
+            cpu = cpu_reference(1 << args.ref_log2t, os.cpu_count() or 1, runs=3)
         except Exception as e:  # noqa: BLE001
             cpu = {"error": str(e)}
 
@@ -353,12 +493,66 @@ def run_psk(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic", "config": config(args),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
         torch.distributed.destroy_process_group()
+
+
+def run_e2e_sharded(args, psk, dist_psk, model, ys, spec, be, stream, rank, world, lo, hi,
+                    T, pg, dev) -> dict:
+    """N > 1: every rank copies its shard's inputs in from pinned host memory,
+    runs the sharded PRTS and copies its shard's smoothed stats out to pinned
+    host memory, synchronously, every step; the step time is the max over
+    ranks (each rank has its own PCIe link, so the copies scale with N)."""
+    import torch
+
+    names = ("f", "u", "q", "h", "d", "r")
+    host = {k: torch.empty(getattr(model, k).shape, dtype=getattr(model, k).dtype,
+                           pin_memory=True) for k in names}
+    for k in names:
+        host[k].copy_(getattr(model, k))
+    host_y = torch.empty(ys.shape, dtype=ys.dtype, pin_memory=True)
+    host_y.copy_(ys)
+    n = hi - lo
+    hm = torch.empty((n, 4), dtype=ys.dtype, pin_memory=True)
+    hc = torch.empty((n, 4, 4), dtype=ys.dtype, pin_memory=True)
+
+    def one():
+        with torch.cuda.stream(stream):
+            for k in names:
+                getattr(model, k).copy_(host[k], non_blocking=True)
+            ys.copy_(host_y, non_blocking=True)
+            out = dist_psk.prts_run_sharded(model, ys, spec, be, rank, world, lo, hi, T, pg)
+            hm.copy_(out.mean, non_blocking=True)
+            hc.copy_(out.cov, non_blocking=True)
+        stream.synchronize()
+        return float(hm[-1, 0])  # the result is on the host
+
+    one()
+    steps = max(2, min(args.steps, 8))
+    ts = []
+    for _ in range(steps):
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        one()
+        ts.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(ts) / len(ts)], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    sec = float(t.item())
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + \
+        host_y.numel() * host_y.element_size()
+    d2h = hm.numel() * hm.element_size() + hc.numel() * hc.element_size()
+    hb = torch.tensor([float(h2d), float(d2h)], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(hb)
+    return {"value": T / sec, "unit": "time-steps/s",
+            "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
+            "steps": steps,
+            "timer": "wall clock per step (barrier, H2D of the shard, sharded PRTS, D2H of "
+                     "the shard's result, host read), max over ranks",
+            "pipelining": "none (one synchronous step at a time per rank)"}
 
 
 def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
@@ -415,17 +609,21 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
     for b in bes:
         b.sync()
     psteps = max(4, min(args.steps, 16))  # fill / drain of the 2-deep pipeline amortised
+    marks = []
     t0 = time.perf_counter()
     for i in range(psteps):
         j = i % 2
         if i >= 2:
             bes[j].sync()
             float(outs[j].mean[-1, 0])  # step i-2's result, on the host
+            marks.append(time.perf_counter() - t0)
         psk.prts_run(m, ys, spec, bes[j], out=outs[j])
     for i in range(psteps - 2, psteps):
         bes[i % 2].sync()
         float(outs[i % 2].mean[-1, 0])
+        marks.append(time.perf_counter() - t0)
     sec = (time.perf_counter() - t0) / psteps
+    done_ms = [round(1e3 * b, 1) for b in marks]  # when each step's result was on the host
     for b in bes:
         b.set_option("async", 0)
     return {"value": T / sec, "unit": "time-steps/s", "h2d_bytes_per_step": int(h2d),
@@ -433,6 +631,7 @@ def run_e2e(args, psk, T, tdt, F, Q, H, R, m0, P0, ys_np, spec, local) -> dict:
             "timer": "wall clock over the step loop (host reads every step's result)",
             "pipelining": "2 contexts, async API: step i's H2D overlaps step i-1's "
                           "kernels + D2H",
+            "result_on_host_ms": done_ms,
             "sync_value": T / sec_sync,
             "sync_note": "one synchronous call at a time (H2D, kernels, D2H in series)",
             "breakdown_ms": {k: round(v, 2) for k, v in br.items()},

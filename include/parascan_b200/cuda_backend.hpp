@@ -127,6 +127,18 @@ constexpr int dtype_of() {
   return std::is_same_v<S, double> ? PSK_F64 : PSK_F32;
 }
 
+// shape checks of one step's block: the reference's mat_mul / mat_add reject
+// mismatched operands with DimensionMismatch (mat.hpp:61-63); the packer
+// memcpys raw blocks, so it checks every block before reading it
+template <typename S>
+inline bool block_dims_ok(const Mat<S>& a, std::size_t r, std::size_t c) {
+  return std::size_t(a.rows()) == r && std::size_t(a.cols()) == c;
+}
+template <typename S>
+inline bool block_dims_ok(const Vec<S>& a, std::size_t r, std::size_t) {
+  return std::size_t(a.len()) == r;
+}
+
 // Lgssm<S> (per-step std::vector<Mat>) -> per-field dense arrays in the
 // backend's pinned input buffer (one field after another, 16-byte aligned)
 template <typename S>
@@ -135,6 +147,8 @@ psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
   if (m.f.size() != t || m.u.size() != t || m.q.size() != t || m.h.size() != t ||
       m.d.size() != t || m.r.size() != t || ys.size() != t)
     throw DimensionMismatch("model / measurement length");
+  if (!block_dims_ok(m.prior_mean, nx, 1) || !block_dims_ok(m.prior_cov, nx, nx))
+    throw DimensionMismatch("prior dims");
   const std::size_t blk[9] = {nx * nx, nx, nx * nx, ny * nx, ny, ny * ny, ny, nx, nx * nx};
   std::size_t off[9], total = 0;
   const std::size_t align = 16 / sizeof(S);
@@ -145,18 +159,22 @@ psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
   }
   S* base = static_cast<S*>(buf.reserve(sizeof(S) * (total ? total : 1)));
   parallel_for(t, 1 << 14, [&](std::size_t lo, std::size_t hi) {
-    auto put = [&](int i, const auto& src) {
+    auto put = [&](int i, const auto& src, std::size_t r, std::size_t c) {
       S* dst = base + off[i];
       const std::size_t b = blk[i];
-      for (std::size_t k = lo; k < hi; ++k) std::memcpy(dst + k * b, src[k].view().d, sizeof(S) * b);
+      for (std::size_t k = lo; k < hi; ++k) {
+        if (!block_dims_ok(src[k], r, c))
+          throw DimensionMismatch("step " + std::to_string(k) + ": block dims");
+        std::memcpy(dst + k * b, src[k].view().d, sizeof(S) * b);
+      }
     };
-    put(0, m.f);
-    put(1, m.u);
-    put(2, m.q);
-    put(3, m.h);
-    put(4, m.d);
-    put(5, m.r);
-    put(6, ys);
+    put(0, m.f, nx, nx);
+    put(1, m.u, nx, 1);
+    put(2, m.q, nx, nx);
+    put(3, m.h, ny, nx);
+    put(4, m.d, ny, 1);
+    put(5, m.r, ny, ny);
+    put(6, ys, ny, 1);
   });
   std::memcpy(base + off[7], m.prior_mean.view().d, sizeof(S) * nx);
   std::memcpy(base + off[8], m.prior_cov.view().d, sizeof(S) * nx * nx);

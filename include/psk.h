@@ -111,6 +111,9 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
  *   "shard_async"  1: the shard phases before psk_shard_smoother_finish and
  *               the folds return without synchronising the stream (errors
  *               are reported by the smoother finish); default 0
+ *   "dlb_trace" 1: diagnostics -- per-phase timestamps of every decoupled
+ *               look-back scan of this context are appended to the file
+ *               $PSK_DLB_TRACE (tools/dlb_trace.py); synchronises each scan
  * Returns PSK_E_ARG for an unknown key or value. */
 int psk_set_option(psk_ctx* ctx, const char* key, int64_t value);
 /* Wait for the context's queued work and report the first device error since
@@ -119,6 +122,9 @@ int psk_sync(psk_ctx* ctx);
 /* Run on this CUDA stream (cudaStream_t as void*; NULL = context stream).
  * The entry points are synchronous: outputs are valid on return. */
 int psk_set_stream(psk_ctx* ctx, void* stream);
+/* The stream the context currently runs on (its own stream unless one was set
+ * with psk_set_stream), so callers can order their own work against it. */
+int psk_get_stream(psk_ctx* ctx, void** stream);
 
 /* Parallel Kalman filter (Alg. 5).  mean[T][nx], cov[T][nx][nx] in
  * model->space, model->dtype. */

@@ -113,6 +113,26 @@ int main() {
     }
     std::printf("indefinite S -> NotPositiveDefinite: %s\n", threw ? "yes" : "no");
     if (!threw) ++bad;
+    // a malformed step block: the reference rejects it in mat_mul
+    // (DimensionMismatch, mat.hpp:61-63); so must the packer
+    Lgssm<double> mb = gen_model(5, 4, 2, 40);
+    const Measurements<double> ysb = simulate_data(mb, 6);
+    mb.h[7] = Mat<double>(3, 4);
+    bool ref_threw = false;
+    threw = false;
+    try {
+      prts_run(mb, ysb, ScanSpec{ScanAlg::InplaceLaFi, 1}, pool);
+    } catch (const DimensionMismatch&) {
+      ref_threw = true;
+    }
+    try {
+      prts_run(mb, ysb, ScanSpec{ScanAlg::InplaceLaFi, 1}, gpu);
+    } catch (const DimensionMismatch&) {
+      threw = true;
+    }
+    std::printf("malformed H block -> DimensionMismatch: reference %s, CudaBackend %s\n",
+                ref_threw ? "yes" : "no", threw ? "yes" : "no");
+    if (!threw || !ref_threw) ++bad;
   }
   std::printf("%s\n", bad ? "DROPIN FAIL" : "DROPIN OK");
   return bad ? 1 : 0;

@@ -36,8 +36,13 @@ class OracleError(RuntimeError):
 
 
 class Flat(C.Structure):
+    # `bcast` (port only; the reference shim's struct ends at p0 and never
+    # reads it): bit i set = field i of f,u,q,h,d,r,y is one time-invariant block
     _fields_ = [("t", C.c_size_t), ("nx", C.c_int), ("ny", C.c_int)] + [
-        (n, C.c_void_p) for n in ("f", "u", "q", "h", "d", "r", "y", "m0", "p0")]
+        (n, C.c_void_p) for n in ("f", "u", "q", "h", "d", "r", "y", "m0", "p0")] + [
+        ("bcast", C.c_uint)]
+
+FIELDS = ("f", "u", "q", "h", "d", "r", "y")
 
 
 def build() -> None:
@@ -45,23 +50,29 @@ def build() -> None:
     subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
 
 
-def dense_fields(m, ys, dtype=np.float64) -> dict:
-    """Per-step dense arrays of a model (time-invariant fields expanded)."""
+def dense_fields(m, ys, dtype=np.float64, keep_bcast: bool = False) -> dict:
+    """Per-step dense arrays of a model.  Time-invariant fields (no step axis)
+    are expanded, or with `keep_bcast` kept as one block and flagged in
+    "bcast" (the port reads them with stride 0)."""
     t, nx, ny = int(m.t), int(m.nx), int(m.ny)
+    flags = [0]
 
-    def exp(a, shp):
+    def exp(i, a, shp):
         a = np.asarray(a.cpu() if hasattr(a, "cpu") else a, dtype=dtype)
         if a.shape == shp:
+            if keep_bcast:
+                flags[0] |= 1 << i
+                return np.ascontiguousarray(a, dtype=dtype)
             a = np.broadcast_to(a, (t, *shp))
         return np.ascontiguousarray(a, dtype=dtype)
 
     return dict(
-        f=exp(m.f, (nx, nx)), u=exp(m.u, (nx,)), q=exp(m.q, (nx, nx)),
-        h=exp(m.h, (ny, nx)), d=exp(m.d, (ny,)), r=exp(m.r, (ny, ny)),
-        y=exp(ys, (ny,)),
+        f=exp(0, m.f, (nx, nx)), u=exp(1, m.u, (nx,)), q=exp(2, m.q, (nx, nx)),
+        h=exp(3, m.h, (ny, nx)), d=exp(4, m.d, (ny,)), r=exp(5, m.r, (ny, ny)),
+        y=exp(6, ys, (ny,)),
         m0=np.ascontiguousarray(np.asarray(m.prior_mean.cpu() if hasattr(m.prior_mean, "cpu") else m.prior_mean, dtype=dtype)),
         p0=np.ascontiguousarray(np.asarray(m.prior_cov.cpu() if hasattr(m.prior_cov, "cpu") else m.prior_cov, dtype=dtype)),
-        t=t, nx=nx, ny=ny)
+        t=t, nx=nx, ny=ny, bcast=flags[0])
 
 
 class Oracle:
@@ -86,6 +97,7 @@ class Oracle:
         fl.t, fl.nx, fl.ny = fd["t"], fd["nx"], fd["ny"]
         for n in ("f", "u", "q", "h", "d", "r", "y", "m0", "p0"):
             setattr(fl, n, fd[n].ctypes.data)
+        fl.bcast = fd.get("bcast", 0)
         return fl
 
     @staticmethod
@@ -99,7 +111,7 @@ class Oracle:
     def _run(self, what: str, m, ys, dtype, *extra, shim_threads: bool = True):
         dtype = np.dtype(dtype)
         sfx = "d" if dtype == np.float64 else "f"
-        fd = dense_fields(m, ys, dtype)
+        fd = dense_fields(m, ys, dtype, keep_bcast=self.which == "port")
         fl = self._flat(fd)
         mean, cov = self._stats(fd, dtype)
         fn = self._fn(what, sfx)
@@ -128,7 +140,7 @@ class Oracle:
         fm, fc = self.kf_run(m, ys, dtype)
         dtype = np.dtype(dtype)
         sfx = "d" if dtype == np.float64 else "f"
-        fd = dense_fields(m, ys, dtype)
+        fd = dense_fields(m, ys, dtype, keep_bcast=True)
         fl = self._flat(fd)
         mean, cov = self._stats(fd, dtype)
         st = self._fn("rts_run", sfx)(C.byref(fl), self._p(fm), self._p(fc),

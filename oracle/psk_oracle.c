@@ -166,18 +166,18 @@ int pso_simulate_data(const pso_model_d* m, uint64_t seed, double* ys) {
   mmul_d(x, l, z, nx, nx, 1);
   madd_d(x, x, m->m0, nx, 1);
   for (size_t k = 0; k < m->t; ++k) {
-    mmul_d(xn, m->f + k * nx * nx, x, nx, nx, 1);
-    madd_d(xn, xn, m->u + k * nx, nx, 1);
+    mmul_d(xn, MF(m, k), x, nx, nx, 1);
+    madd_d(xn, xn, MU(m, k), nx, 1);
     gs_init(&g, stream_seed(seed, k, kRoleStateNoise));
-    if (chol_d(l, m->q + k * nx * nx, nx)) return PSO_E_NOT_PD;
+    if (chol_d(l, MQ(m, k), nx)) return PSO_E_NOT_PD;
     gs_fill(&g, z, nx);
     mmul_d(nn, l, z, nx, nx, 1);
     madd_d(xn, xn, nn, nx, 1);
     mcopy_d(x, xn, nx, 1);
-    mmul_d(y, m->h + k * ny * nx, x, ny, nx, 1);
-    madd_d(y, y, m->d + k * ny, ny, 1);
+    mmul_d(y, MH(m, k), x, ny, nx, 1);
+    madd_d(y, y, MD(m, k), ny, 1);
     gs_init(&g, stream_seed(seed, k, kRoleMeasNoise));
-    if (chol_d(l, m->r + k * ny * ny, ny)) return PSO_E_NOT_PD;
+    if (chol_d(l, MR(m, k), ny)) return PSO_E_NOT_PD;
     gs_fill(&g, z, ny);
     mmul_d(nn, l, z, ny, ny, 1);
     madd_d(y, y, nn, ny, 1);

@@ -50,6 +50,7 @@ extern "C" {
     size_t t;                                                                 \
     int nx, ny;                                                               \
     const S *f, *u, *q, *h, *d, *r, *y, *m0, *p0;                             \
+    unsigned bcast; /* bit i: field i (f,u,q,h,d,r,y) is one block */         \
   } pso_model_##SFX;                                                          \
   int pso_kf_run_##SFX(const pso_model_##SFX* m, S* mean, S* cov);            \
   int pso_rts_run_##SFX(const pso_model_##SFX* m, const S* fmean,             \

@@ -46,6 +46,7 @@ SIGNATURES = {
     "psk_set_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "psk_set_chunk": (C.c_int, [C.c_void_p, C.c_int]),
     "psk_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "psk_get_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "psk_sync": (C.c_int, [C.c_void_p]),
     "psk_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "psk_pkf": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int, C.c_uint64,

@@ -165,6 +165,8 @@ class CudaBackend:
         _check(L.psk_create(C.byref(ctx), int(device)))
         self._ctx = ctx
         self.device = int(device)
+        self._async = False
+        self._pending: list[Any] = []  # marshals alive until sync() (async mode)
         self.set_mode(mode)
         self.set_chunk(chunk)
         if stream is not None:
@@ -173,10 +175,15 @@ class CudaBackend:
     def sync(self) -> None:
         """Wait for queued work; raise the first device error since the last
         synchronising call (async mode, option "async")."""
-        _check(_lib.lib().psk_sync(self._ctx))
+        try:
+            _check(_lib.lib().psk_sync(self._ctx))
+        finally:
+            self._pending.clear()
 
     def set_option(self, key: str, value: int) -> None:
         _check(_lib.lib().psk_set_option(self._ctx, key.encode(), int(value)))
+        if key == "async":
+            self._async = bool(value)
 
     # reference Backend interface: host closures cannot run on the device
     def run(self, launch: Any) -> None:  # backend.hpp:42
@@ -205,6 +212,12 @@ class CudaBackend:
         else:
             handle = getattr(stream, "cuda_stream", stream) or 1
         _check(_lib.lib().psk_set_stream(self._ctx, C.c_void_p(handle)))
+
+    def stream_handle(self) -> int:
+        """The cudaStream_t the context runs on (psk_get_stream)."""
+        h = C.c_void_p()
+        _check(_lib.lib().psk_get_stream(self._ctx, C.byref(h)))
+        return int(h.value or 0)
 
     def set_profile(self, on: bool) -> None:
         _check(_lib.lib().psk_set_profile(self._ctx, int(bool(on))))
@@ -341,28 +354,103 @@ def _validate(m: Lgssm) -> None:
         raise DimensionMismatch("mat dims")
 
 
+def _check_out(mk: _Marshal, a: Any, shape: tuple) -> None:
+    """A caller-provided output buffer must match the model: shape, dtype,
+    C-contiguity and memory kind (CUDA tensors on the inputs' device for a
+    device-space model, host memory otherwise) -- the library writes
+    shape x dtype bytes of raw row-major data through its pointer."""
+    if tuple(a.shape) != shape:
+        raise DimensionMismatch(f"output buffer shape {tuple(a.shape)}, expected {shape}")
+    if mk.torch:
+        import torch
+        if not _is_torch(a):
+            raise ValueError("outputs must be torch tensors like the inputs")
+        if a.dtype != (torch.float64 if mk.f64 else torch.float32):
+            raise DimensionMismatch(f"output dtype {a.dtype} differs from the model's")
+        if not a.is_contiguous():
+            raise ValueError("output buffers must be contiguous")
+        if mk.device is not None and a.device != mk.device:
+            raise ValueError(f"outputs on {a.device}, inputs on {mk.device}")
+        if mk.device is None and a.device.type != "cpu":
+            raise ValueError("host-space model: outputs must be host (CPU) tensors")
+    else:
+        if not isinstance(a, np.ndarray):
+            raise ValueError("outputs must be numpy arrays like the inputs")
+        if a.dtype != (np.float64 if mk.f64 else np.float32):
+            raise DimensionMismatch(f"output dtype {a.dtype} differs from the model's")
+        if not a.flags.c_contiguous or not a.flags.writeable:
+            raise ValueError("output buffers must be C-contiguous and writeable")
+
+
+def _outputs(mk: _Marshal, out: GaussianStats | None) -> tuple[Any, Any]:
+    if out is None:
+        return mk.outputs()
+    _check_out(mk, out.mean, (mk.t, mk.nx))
+    _check_out(mk, out.cov, (mk.t, mk.nx, mk.nx))
+    return out.mean, out.cov
+
+
+def _ordered_call(bes: list[CudaBackend], mks: list[_Marshal], outs: list[Any], call) -> None:
+    """Run `call` (one C-ABI entry) ordered against torch's current stream.
+
+    The contexts run on their own streams.  For device-space (CUDA tensor)
+    models their streams first wait for torch's current stream (inputs and the
+    contiguous copies _Marshal made are produced there), torch's stream then
+    waits for theirs (the outputs), and every tensor the call reads or writes
+    is recorded on the context streams so the caching allocator cannot hand
+    its memory out while a queued (async mode) kernel still uses it.  Host
+    marshals of async calls are kept alive until sync()."""
+    dev = next((mk.device for mk in mks if mk.device is not None), None)
+    if dev is None:
+        call()
+        for be in bes:
+            if be._async:
+                be._pending.append(mks)
+        return
+    import torch
+    cur = torch.cuda.current_stream(dev)
+    exts = []
+    for be in bes:
+        h = be.stream_handle()
+        if h not in (cur.cuda_stream, 0):
+            ext = torch.cuda.ExternalStream(h, device=torch.device("cuda", be.device))
+            ext.wait_stream(cur)
+            exts.append(ext)
+    call()
+    for ext in exts:
+        cur.wait_stream(ext)
+        for mk in mks:
+            for t in mk.keep:
+                if _is_torch(t) and t.device.type == "cuda":
+                    t.record_stream(ext)
+        for t in outs:
+            if t.device.type == "cuda":
+                t.record_stream(ext)
+
+
 def _run(entry: str, m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,
          be_bwd: CudaBackend | None = None, devices: int = 1,
          out: GaussianStats | None = None) -> GaussianStats:
     _validate(m)
     mk = _Marshal(m, ys)
-    if out is None:
-        mean, cov = mk.outputs()
-    else:  # caller-provided buffers (e.g. pinned host memory), same kind as inputs
-        mean, cov = out.mean, out.cov
-        if tuple(mean.shape) != (mk.t, mk.nx) or tuple(cov.shape) != (mk.t, mk.nx, mk.nx):
-            raise DimensionMismatch("output buffer shapes")
+    mean, cov = _outputs(mk, out)
     L = _lib.lib()
     pm = C.c_void_p(mk._ptr(mean))
     pc = C.c_void_p(mk._ptr(cov))
     if entry == "ptfs":
-        st = L.psk_ptfs(be.handle, (be_bwd or be).handle, int(devices),
-                        C.byref(mk.model), int(spec.alg), int(spec.sengupta_n), pm, pc)
+        bes = [be] if be_bwd is None or be_bwd is be else [be, be_bwd]
+
+        def call():
+            _check(L.psk_ptfs(be.handle, (be_bwd or be).handle, int(devices),
+                              C.byref(mk.model), int(spec.alg), int(spec.sengupta_n), pm, pc))
     else:
+        bes = [be]
         fn = L.psk_pkf if entry == "pkf" else L.psk_prts
-        st = fn(be.handle, C.byref(mk.model), int(spec.alg), int(spec.sengupta_n),
-                pm, pc)
-    _check(st)
+
+        def call():
+            _check(fn(be.handle, C.byref(mk.model), int(spec.alg), int(spec.sengupta_n),
+                      pm, pc))
+    _ordered_call(bes, [mk], [mean, cov] if mk.torch else [], call)
     return GaussianStats(mean, cov)
 
 
@@ -393,20 +481,22 @@ def _run_batch(entry: str, models: list[Lgssm], ys_list: list[Any], spec: ScanSp
     for i, (m, ys) in enumerate(zip(models, ys_list)):
         _validate(m)
         mk = _Marshal(m, ys)
-        if outs is None:
-            mean, cov = mk.outputs()
-        else:
-            mean, cov = outs[i].mean, outs[i].cov
-            if tuple(mean.shape) != (mk.t, mk.nx) or tuple(cov.shape) != (mk.t, mk.nx, mk.nx):
-                raise DimensionMismatch("output buffer shapes")
+        mean, cov = _outputs(mk, None if outs is None else outs[i])
         mks.append(mk)
         res.append(GaussianStats(mean, cov))
+    devs = {mk.device for mk in mks}
+    if len(devs) > 1:
+        raise ValueError("a batch must be all host-space or all on one CUDA device")
     n = len(mks)
     arr = (_lib.psk_model * max(n, 1))(*[mk.model for mk in mks])
     pm = (C.c_void_p * max(n, 1))(*[mks[i]._ptr(res[i].mean) for i in range(n)])
     pc = (C.c_void_p * max(n, 1))(*[mks[i]._ptr(res[i].cov) for i in range(n)])
     fn = _lib.lib().psk_pkf_batch if entry == "pkf" else _lib.lib().psk_prts_batch
-    _check(fn(be.handle, arr, n, int(spec.alg), int(spec.sengupta_n), pm, pc))
+
+    def call():
+        _check(fn(be.handle, arr, n, int(spec.alg), int(spec.sengupta_n), pm, pc))
+    tens = [t for r in res for t in (r.mean, r.cov)] if mks and mks[0].torch else []
+    _ordered_call([be], mks, tens, call)
     return res
 
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -604,25 +605,48 @@ int ptfs_two_typed(psk_ctx* cf, psk_ctx* cb, const psk_model* m, int alg, uint64
   const int nx = m->nx;
   ModelView<S> va, vb;
   int st;
+  // device-space inputs that live on another GPU than a context are staged
+  // like host inputs on that context (no peer access is assumed)
+  auto foreign = [&](int dev) {
+    if (m->space != PSK_DEVICE) return false;
+    cudaPointerAttributes at{};
+    const void* fields[9] = {m->f, m->u, m->q, m->h, m->d, m->r, m->y, m->prior_mean,
+                             m->prior_cov};
+    for (const void* p : fields) {
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (at.type == cudaMemoryTypeDevice && at.device != dev) return true;
+    }
+    return false;
+  };
   {
     DeviceGuard dg(cb->device);
-    int dev = -1;
-    cudaPointerAttributes at{};
-    const bool foreign = m->space == PSK_DEVICE &&
-                         cudaPointerGetAttributes(&at, m->f) == cudaSuccess &&
-                         at.type == cudaMemoryTypeDevice && at.device != cb->device;
-    (void)dev;
-    st = prepare_model<S>(cb, m, vb, 0, foreign);
+    st = prepare_model<S>(cb, m, vb, 0, foreign(cb->device));
     if (st) return st;
   }
   DeviceGuard dg(cf->device);
-  st = prepare_model<S>(cf, m, va);
+  st = prepare_model<S>(cf, m, va, 0, foreign(cf->device));
   if (st) return st;
   const bool host = m->space == PSK_HOST;
   const size_t mb = sizeof(S) * (size_t)T * nx, cb_ = sizeof(S) * (size_t)T * nx * nx;
   S* dmean = static_cast<S*>(mean);
   S* dcov = static_cast<S*>(cov);
-  const bool tmp_out = host || !aligned16(mean) || !aligned16(cov);
+  // device outputs on another GPU than the forward context are written
+  // through a staging buffer on it (cudaMemcpyDefault resolves the pair)
+  bool out_foreign = false;
+  if (!host) {
+    for (void* p : {mean, cov}) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, p) == cudaSuccess) {
+        if (at.type == cudaMemoryTypeDevice && at.device != cf->device) out_foreign = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
+  const bool tmp_out = host || out_foreign || !aligned16(mean) || !aligned16(cov);
   if (tmp_out) {
     dmean = static_cast<S*>(ctx_alloc(mb + 16, cf));
     dcov = static_cast<S*>(ctx_alloc(cb_ + 16, cf));
@@ -744,6 +768,7 @@ int psk_destroy(psk_ctx* c) {
     for (auto s : c->sub) cudaStreamDestroy(s);
     for (auto e : c->sub_ev) cudaEventDestroy(e);
     cudaFree(c->d_err);
+    if (c->launch.dlb_trace) cudaFree(c->launch.dlb_trace);
     cudaStreamDestroy(c->own_stream);
   }
   delete c;
@@ -779,6 +804,25 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   } else if (k == "batch_streams") {
     if (value < 1 || value > 64) return fail(PSK_E_ARG, "batch_streams must be 1..64");
     c->batch_streams = (int)value;
+  } else if (k == "dlb_trace") {
+    // diagnostics: per-phase stamps of every DLB scan of this context are
+    // appended to $PSK_DLB_TRACE (default dlb_trace.bin); synchronises
+    if (value != 0 && value != 1) return fail(PSK_E_ARG, "dlb_trace must be 0 or 1");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    if (value && !c->launch.dlb_trace) {
+      const long long cap = 65536;
+      if (cudaMalloc(&c->launch.dlb_trace, sizeof(unsigned long long) * 8 * cap) != cudaSuccess)
+        return fail(PSK_E_ALLOC, "trace buffer");
+      c->launch.dlb_trace_cap = cap;
+      const char* path = std::getenv("PSK_DLB_TRACE");
+      c->launch.dlb_trace_path = path ? path : "dlb_trace.bin";
+    } else if (!value && c->launch.dlb_trace) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(c->launch.dlb_trace);
+      c->launch.dlb_trace = nullptr;
+      c->launch.dlb_trace_cap = 0;
+    }
   } else if (k == "waves") {
     if (value < 1 || value > 1024) return fail(PSK_E_ARG, "waves must be 1..1024");
     c->waves = (int)value;
@@ -820,6 +864,12 @@ int psk_sync(psk_ctx* c) {
 int psk_set_stream(psk_ctx* c, void* stream) {
   if (!c) return fail(PSK_E_ARG, "null context");
   c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return PSK_OK;
+}
+
+int psk_get_stream(psk_ctx* c, void** stream) {
+  if (!c || !stream) return fail(PSK_E_ARG, "null context or stream out");
+  *stream = static_cast<void*>(c->stream);
   return PSK_OK;
 }
 

@@ -304,20 +304,14 @@ void dlb_scan(ExactLaunch& L, const Ops& ops, typename Ops::S* buf, long long n,
   const int per = dlb_per<Ops>(n);
   const long long ntiles = dlb_tiles(n, per);
   cudaMemsetAsync(state, 0, dlb_head_bytes(ntiles), L.stream);
-  static unsigned long long* trace = nullptr;  // PSK_DLB_TRACE: stamps of the last scan
-  static long long trace_tiles = 0;
-  if (std::getenv("PSK_DLB_TRACE") != nullptr) {
-    if (trace == nullptr) cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 65536);
-    trace_tiles = ntiles;
-  }
+  unsigned long long* trace = ntiles <= L.dlb_trace_cap ? L.dlb_trace : nullptr;
   k_dlb<Ops><<<(unsigned)ntiles, kDlbThreads, smem, L.stream>>>(
-      ops, buf, n, cap, rev, perm, reinterpret_cast<char*>(state), ntiles, per,
-      trace != nullptr && ntiles <= 65536 ? trace : nullptr);
-  if (trace != nullptr && std::getenv("PSK_DLB_TRACE") != nullptr) {
-    std::vector<unsigned long long> h((size_t)trace_tiles * 8);
+      ops, buf, n, cap, rev, perm, reinterpret_cast<char*>(state), ntiles, per, trace);
+  if (trace != nullptr) {  // diagnostics only: synchronises the stream
+    std::vector<unsigned long long> h((size_t)ntiles * 8);
     cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, L.stream);
     cudaStreamSynchronize(L.stream);
-    FILE* f = std::fopen(std::getenv("PSK_DLB_TRACE"), "ab");
+    FILE* f = std::fopen(L.dlb_trace_path.c_str(), "ab");
     if (f) {
       const long long hdr[4] = {ntiles, per, (long long)Ops::kSize, n};
       std::fwrite(hdr, sizeof(hdr), 1, f);

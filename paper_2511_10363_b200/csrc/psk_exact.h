@@ -5,6 +5,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <string>
 #include <vector>
 
 #include "psk_common.cuh"
@@ -57,6 +58,11 @@ struct ExactLaunch {
   std::vector<cudaEvent_t> evs;  // evs[0] = start; kernel i ends at evs[i+1]
   // async mode: the event spans of calls not yet synchronised
   std::vector<std::pair<std::vector<cudaEvent_t>, std::vector<const char*>>> pending;
+  // optional DLB phase trace of this context (option "dlb_trace"; stamps of
+  // every scan are appended to trace_path, read by tools/dlb_trace.py)
+  unsigned long long* dlb_trace = nullptr;
+  long long dlb_trace_cap = 0;  // tiles
+  std::string dlb_trace_path;
   void start(bool keep = false) {
     launches = 0;
     if (keep && !evs.empty()) {

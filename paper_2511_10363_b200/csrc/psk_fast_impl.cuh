@@ -27,6 +27,19 @@ inline int grid_for(long long n, int block) {
 constexpr int kBlock = 128;
 }  // namespace
 
+// Let device `dev` read / copy from `peer` over NVLink when the pair supports
+// it (idempotent; the copy falls back to staging through the host otherwise).
+inline void enable_peer(int dev, int peer) {
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();  // clear the sticky-free error
+  cudaSetDevice(cur);
+}
+
 // The model shifted by one step (step i of the view = step i + 1 of m,
 // t - 1 steps, no prior): the backward pass of PTFS walks the elements
 // a(step i+1) at slot i.
@@ -435,9 +448,16 @@ static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, Exact
   st = fast_phase_t<S, NX, NY>(LB, mB, a, sb, 4, nullptr, nullptr, nullptr, nullptr);
   if (st) return st;
   cudaEvent_t done_b;
-  cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming);
+  if (cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming) != cudaSuccess) return 7;
+  // destroyed on every path below (an event still pending in a stream wait is
+  // released by the runtime once the wait completes)
+  struct EventGuard {
+    cudaEvent_t e;
+    ~EventGuard() { cudaEventDestroy(e); }
+  } guard{done_b};
   cudaEventRecord(done_b, LB.stream);
   cudaSetDevice(devA);
+  if (devA != devB) enable_peer(devA, devB);  // NVLink P2P for the element copy
   st = fast_prepare_t<S, NX, NY>(mA, a, sa, allocA, ctxA);
   if (st) return st;
   st = fast_phase_t<S, NX, NY>(LA, mA, a, sa, 0, mean, cov, nullptr, nullptr);
@@ -446,14 +466,10 @@ static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, Exact
   // the forward elements in sa.agg are dead after the forward finish
   cudaStreamWaitEvent(LA.stream, done_b, 0);
   // both sides hold the backward elements in the same slot order
-  if (sa.cap != sb.cap || sa.bord.per != sb.bord.per) {
-    cudaEventDestroy(done_b);
-    return 7;
-  }
+  if (sa.cap != sb.cap || sa.bord.per != sb.bord.per) return 7;
   cudaMemcpyPeerAsync(sa.agg, devA, sb.agg, devB,
                       sizeof(S) * FLayout<NX>::size * (size_t)sa.cap, LA.stream);
   LA.count("ptfs_backward_elements_peer_copy");
-  cudaEventDestroy(done_b);
   return fast_phase_t<S, NX, NY>(LA, mA, a, sa, 5, mean, cov, nullptr, nullptr);
 }
 

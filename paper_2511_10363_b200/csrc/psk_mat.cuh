@@ -40,29 +40,41 @@ __device__ __forceinline__ S sabs(S x) {
 // correctly rounded square root (exact mode: bitwise with the reference)
 __device__ __forceinline__ double ssqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float ssqrt(float x) { return sqrtf(x); }
+// The FP64 MUFU seeds flush subnormal inputs and results to zero (only .ftz
+// variants exist), where the reference divides in IEEE: inputs whose
+// reciprocal (or reciprocal root) would leave the normal range are scaled by a
+// power of two first and the result scaled back (selects, no branch), so a
+// subnormal pivot gives the finite IEEE quotient, not inf.
 __device__ __forceinline__ double srcp(double x) {
+  const double ax = fabs(x);
+  const double s = ax < 0x1p-1000 ? 0x1p+64 : (ax > 0x1p+1000 ? 0x1p-64 : 1.0);
+  const double xs = x * s;
   double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xs));
+  double e = fma(-xs, r, 1.0);
   r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  e = fma(-xs, r, 1.0);
+  return fma(r, e, r) * s;
 }
 __device__ __forceinline__ float srcp(float x) {
   float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));  // no .ftz: subnormals kept
   return fmaf(r, fmaf(-x, r, 1.0f), r);
 }
 __device__ __forceinline__ double srsqrt(double x) {
+  // x < 2^-1000: rsqrt(x 2^128) 2^64
+  const bool tiny = x < 0x1p-1000;
+  const double xs = tiny ? x * 0x1p+128 : x;
   double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double h = 0.5 * x;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xs));
+  const double h = 0.5 * xs;
   r = fma(r, fma(-h * r, r, 0.5), r);
-  return fma(r, fma(-h * r, r, 0.5), r);
+  r = fma(r, fma(-h * r, r, 0.5), r);
+  return tiny ? r * 0x1p+64 : r;
 }
 __device__ __forceinline__ float srsqrt(float x) {
   float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("rsqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
   const float h = 0.5f * x;
   return fmaf(r, fmaf(-h * r, r, 0.5f), r);
 }

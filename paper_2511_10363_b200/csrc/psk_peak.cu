@@ -59,3 +59,38 @@ int run(int device, double* tflops, double* ms_out) {
 extern "C" int psk_peak_fma(int device, int f64, double* tflops, double* ms) {
   return f64 ? run<double>(device, tflops, ms) : run<float>(device, tflops, ms);
 }
+
+// ---- device reciprocal checks (tests/test_gpu_numerics.py) -----------------
+// The fast path's branch-free srcp / srsqrt (psk_mat.cuh) over host arrays, so
+// a test can hold them to the IEEE quotient the reference computes, including
+// subnormal and huge arguments.
+#include "psk_mat.cuh"
+
+namespace {
+template <typename T>
+__global__ void k_rcp(const T* x, T* r, T* q, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    r[i] = psk::srcp(x[i]);
+    q[i] = psk::srsqrt(x[i]);
+  }
+}
+template <typename T>
+int rcp_run(const void* x, void* r, void* q, int n) {
+  T *dx, *dr, *dq;
+  const size_t b = sizeof(T) * (size_t)(n > 0 ? n : 1);
+  if (cudaMalloc(&dx, b) || cudaMalloc(&dr, b) || cudaMalloc(&dq, b)) return 8;
+  cudaMemcpy(dx, x, sizeof(T) * n, cudaMemcpyHostToDevice);
+  k_rcp<T><<<(n + 127) / 128 > 0 ? (n + 127) / 128 : 1, 128>>>(dx, dr, dq, n);
+  cudaMemcpy(r, dr, sizeof(T) * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(q, dq, sizeof(T) * n, cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dr);
+  cudaFree(dq);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+}  // namespace
+
+extern "C" int psk_tool_rcp(int f64, const void* x, void* rcp, void* rsqrt, int n) {
+  return f64 ? rcp_run<double>(x, rcp, rsqrt, n) : rcp_run<float>(x, rcp, rsqrt, n);
+}

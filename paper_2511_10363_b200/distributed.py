@@ -132,6 +132,37 @@ def prts_sharded(engine, spec, rank: int, world: int, t_shard: int, group: Any =
     return mean, cov
 
 
+def shard_model(model, ys, lo: int, hi: int, device: Any = None, dtype: Any = None):
+    """The shard [lo, hi) of a T-step model as device tensors: per-step fields
+    sliced to [lo, min(hi + 1, T)) -- f/u/q carry the one extra transition the
+    smoother boundary needs, h/d/r/y the matching steps (the extra step is
+    never read as a measurement) -- and time-invariant fields kept as one
+    block.  Returns (Lgssm, ys)."""
+    import numpy as np
+    import torch
+
+    from .api import Lgssm
+
+    t = int(model.t)
+    hi_in = min(hi + 1, t)
+    nx, ny = model.nx, model.ny
+    shapes = {"f": (nx, nx), "u": (nx,), "q": (nx, nx), "h": (ny, nx), "d": (ny,),
+              "r": (ny, ny)}
+
+    def put(a, shp=None):
+        x = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
+        if shp is not None and tuple(x.shape) != shp:  # per-step field
+            x = x[lo:hi_in]
+        x = x.to(device=device, dtype=dtype or x.dtype).contiguous()
+        return x
+
+    fields = {k: put(getattr(model, k), shp) for k, shp in shapes.items()}
+    m = Lgssm(**fields, prior_mean=put(model.prior_mean), prior_cov=put(model.prior_cov),
+              t=hi_in - lo)
+    y = ys if isinstance(ys, torch.Tensor) else torch.as_tensor(np.asarray(ys))
+    return m, put(y[lo:hi_in])
+
+
 def shard_flags(rank: int, world: int) -> int:
     return (_lib.PSK_SHARD_FIRST if rank == 0 else 0) | \
         (_lib.PSK_SHARD_LAST if rank == world - 1 else 0)

@@ -146,3 +146,25 @@ def test_batch_validation_without_device():
     assert L.psk_pkf_batch(None, arr, 2, 5, 3, pm, pc) == _lib.PSK_E_CONTRACT  # SenguptaB n=3
     assert L.psk_prts_batch(None, arr, -1, 6, 1, pm, pc) == _lib.PSK_E_ARG
     assert L.psk_prts_batch(None, arr, 2, 6, 1, pm, pc) == _lib.PSK_E_ARG  # null context
+
+
+def test_out_buffer_validation_without_device():
+    """Caller-provided outputs are checked against the model before any
+    pointer is taken: dtype, contiguity, kind of memory."""
+    import numpy as np
+
+    from paper_2511_10363_b200.api import DimensionMismatch, _check_out, _Marshal
+    from paper_2511_10363_b200.synthetic import cv_model
+
+    m, ys = cv_model(8, seed=0)
+    mk = _Marshal(m, ys)
+    _check_out(mk, np.empty((8, 4)), (8, 4))
+    with pytest.raises(DimensionMismatch):
+        _check_out(mk, np.empty((8, 4), np.float32), (8, 4))
+    with pytest.raises(DimensionMismatch):
+        _check_out(mk, np.empty((8, 5)), (8, 4))
+    with pytest.raises(ValueError):
+        _check_out(mk, np.empty((8, 8))[:, ::2], (8, 4))
+    import torch
+    with pytest.raises(ValueError):
+        _check_out(mk, torch.empty(8, 4, dtype=torch.float64), (8, 4))

@@ -1,0 +1,81 @@
+"""The multi-process time-sharded PRTS exactly as bench.py runs it -- the real
+distributed.prts_run_sharded with the CUDA shard engine (CudaShardEngine,
+shard_async on torch's stream) and a real torch.distributed all_gather -- in
+2 and 3 processes that share the one GPU of the test box (NCCL refuses two
+ranks on one device, so the collective is gloo on CUDA tensors here; the bench
+uses NCCL over NVLink).  The concatenated shard outputs must match the CPU
+oracle's sequential rts_run over all T = 2^20 steps at the FP64 gate
+(kalman_par.hpp:156-179 prts_run vs kalman_seq.hpp rts_run)."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import max_rel_err
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+T = 1 << 20
+
+
+def _worker(rank, world, port, out_dir, alg):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200 import distributed as dp
+    from paper_2511_10363_b200.synthetic import cv_model
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    m, ys = cv_model(T, seed=21)
+    lo, hi = dp.shard_range(T, rank, world)
+    ms, yss = dp.shard_model(m, ys, lo, hi, device=dev)
+    be = psk.CudaBackend(0, mode="fast")
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        out = dp.prts_run_sharded(ms, yss, psk.ScanSpec(psk.ScanAlg(alg), 16), be, rank,
+                                  world, lo, hi, T, dist.group.WORLD)
+    torch.cuda.synchronize()
+    np.savez(Path(out_dir) / f"r{rank}.npz", mean=out.mean.cpu().numpy(),
+             cov=out.cov.cpu().numpy(), lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def rts_ref(port):
+    from paper_2511_10363_b200.synthetic import cv_model
+    m, ys = cv_model(T, seed=21)
+    return port.rts_run(m, ys)
+
+
+@pytest.mark.parametrize("world,alg", [(2, 6), (3, 3)])
+def test_prts_run_sharded_processes(gpu, tmp_path, rts_ref, world, alg):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), alg), nprocs=world, join=True)
+    rm, rc = rts_ref
+    covered = 0
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        lo, hi = int(d["lo"]), int(d["hi"])
+        assert lo == covered
+        covered = hi
+        e = max_rel_err(d["mean"], d["cov"], rm[lo:hi], rc[lo:hi])
+        assert e < 1e-9, (r, e)
+    assert covered == T

@@ -150,3 +150,27 @@ def test_shard_range_partition():
             assert spans[0][0] == 0 and spans[-1][1] == t
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+
+
+def test_shard_model_slices_with_boundary_transition():
+    """distributed.shard_model: per-step fields cover [lo, hi + 1) (the
+    smoother boundary transition) except on the last shard; time-invariant
+    fields stay one block; the prior is passed through."""
+    import torch
+
+    from paper_2511_10363_b200.api import Lgssm
+    from paper_2511_10363_b200.distributed import shard_model
+    t = 10
+    f = np.arange(t * 4, dtype=np.float64).reshape(t, 2, 2)
+    m = Lgssm(f=f, u=np.zeros(2), q=np.eye(2), h=np.ones((t, 1, 2)), d=np.zeros(1),
+              r=np.eye(1), prior_mean=np.zeros(2), prior_cov=np.eye(2), t=t)
+    ys = np.arange(t, dtype=np.float64).reshape(t, 1)
+    ms, yss = shard_model(m, ys, 3, 6)
+    assert ms.t == 4 and tuple(ms.f.shape) == (4, 2, 2) and tuple(ms.h.shape) == (4, 1, 2)
+    assert torch.equal(ms.f, torch.as_tensor(f[3:7]))
+    assert tuple(ms.u.shape) == (2,) and tuple(ms.q.shape) == (2, 2)
+    assert torch.equal(yss, torch.as_tensor(ys[3:7]))
+    ml, ysl = shard_model(m, ys, 6, 10)  # last shard: no extra transition
+    assert ml.t == 4 and torch.equal(ml.f, torch.as_tensor(f[6:10]))
+    m32, _ = shard_model(m, ys, 0, 5, dtype=torch.float32)
+    assert m32.f.dtype == torch.float32
