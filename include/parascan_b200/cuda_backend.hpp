@@ -101,6 +101,16 @@ class CudaBackend final : public Backend {
     psk_detail::check(psk_set_mode(ctx_, mode));
     psk_detail::check(psk_set_chunk(ctx_, chunk));
   }
+  // several GPUs (psk_create_multi): pkf_run / prts_run shard the time axis
+  // over them, ptfs_run(m, ys, spec, be, be, devices > 1) runs the forward and
+  // backward filters on the two halves, each time-sharded
+  explicit CudaBackend(const std::vector<int>& devices, int mode = PSK_MODE_FAST,
+                       int chunk = 0) {
+    psk_detail::check(psk_create_multi(&ctx_, devices.data(), int(devices.size())));
+    psk_detail::check(psk_set_mode(ctx_, mode));
+    psk_detail::check(psk_set_chunk(ctx_, chunk));
+  }
+  int devices() const { return psk_num_devices(ctx_); }
   ~CudaBackend() override { psk_destroy(ctx_); }
   CudaBackend(const CudaBackend&) = delete;
   CudaBackend& operator=(const CudaBackend&) = delete;

@@ -94,6 +94,21 @@ typedef struct psk_ctx psk_ctx;
 /* Create a context bound to CUDA device `device` (no host fallback: fails
  * with PSK_E_CUDA when no device is present). */
 int psk_create(psk_ctx** ctx, int device);
+/* A context over several devices (devices[0..ndev), repeats allowed: two
+ * entries of one GPU are two streams of it).  On it psk_pkf / psk_prts shard
+ * the time axis over the devices (shard reduce, exchange of the shard
+ * elements by peer copies over NVLink, fold, finish -- the single-process
+ * form of distributed.py), psk_ptfs runs the forward filter on the first half
+ * of the devices and the backward filter on the second half, each
+ * time-sharded (ptfs_run's devices, kalman_par.hpp:207-211, extended from
+ * {1, 2} to halves), and the batch calls give each device a contiguous share
+ * of the series.  Host inputs are copied shard by shard by the device that
+ * owns the shard.  Calls are synchronous; dimensions without shard phases
+ * (nx or ny > 4), exact mode and series shorter than the shard count run on
+ * the first device.  Replaces: tools/bench_main.cpp:125-128 devices check. */
+int psk_create_multi(psk_ctx** ctx, const int* devices, int ndev);
+/* number of devices of a context (1 for psk_create) */
+int psk_num_devices(psk_ctx* ctx);
 int psk_destroy(psk_ctx* ctx);
 /* Mode and tuning: mode (psk_mode), chunk length (>= 1, or 0 = auto) */
 int psk_set_mode(psk_ctx* ctx, int mode);
@@ -111,6 +126,9 @@ int psk_set_chunk(psk_ctx* ctx, int chunk);
  *   "shard_async"  1: the shard phases before psk_shard_smoother_finish and
  *               the folds return without synchronising the stream (errors
  *               are reported by the smoother finish); default 0
+ *   "tile"      1 (default): state dimensions with a register-tiled warp
+ *               instantiation (nx = 16, ny = 8) run it; 0: the runtime-
+ *               dimension warp kernels (A/B comparisons)
  *   "dlb_trace" 1: diagnostics -- per-phase timestamps of every decoupled
  *               look-back scan of this context are appended to the file
  *               $PSK_DLB_TRACE (tools/dlb_trace.py); synchronises each scan
@@ -173,6 +191,9 @@ int psk_prts_batch(psk_ctx* ctx, const psk_model* models, int count, int alg,
  * (gathered by the caller, e.g. an NCCL all_gather) and their folds. */
 #define PSK_SHARD_FIRST 1
 #define PSK_SHARD_LAST 2
+/* PKF shards (and the forward half of a sharded PTFS): the filter finish
+ * writes the shard's filtered stats to mean / cov and reports errors */
+#define PSK_SHARD_FILTERED 4
 /* filter pass, part 1: local element build + scan; elem_out = shard total */
 int psk_shard_filter_reduce(psk_ctx* ctx, const psk_model* shard, int flags,
                             int alg, uint64_t sengupta_n, void* elem_out);
@@ -196,6 +217,28 @@ int psk_fold_filter(psk_ctx* ctx, int dtype, int nx, const void* elems,
                     int count, void* state_out);
 int psk_fold_smoother(psk_ctx* ctx, int dtype, int nx, const void* elems,
                       int count, void* state_out);
+
+/* ---- time-sharded PTFS (ptfs_run on disjoint GPU halves, kalman_par.hpp:
+ * 207-238): the forward filter runs as a sharded PKF
+ * (PSK_SHARD_FILTERED) on one half of the GPUs while the backward filter runs
+ * sharded on the other half, shard for shard over the same step ranges.  A
+ * backward shard carries one extra step of EVERY field (slot i holds the
+ * element of step i+1, kalman_par.hpp:63-89) unless it is the LAST.
+ *   backward reduce: shifted elements + reverse scan; elem_out = the shard's
+ *     backward total (filter element, later steps on the right);
+ *   psk_fold_backward: e_0 (x) ... (x) e_{count-1} of the LATER shards'
+ *     totals -> (eta | J), nx + nx^2 scalars (the backward information of
+ *     every step after the shard);
+ *   backward finish: from carry (eta | J; NULL for the LAST shard) and the
+ *     shard's filtered stats fmean / fcov (device, from the forward half),
+ *     the smoothed stats (two-filter combination, kalman_seq.hpp:239-260). */
+int psk_shard_backward_reduce(psk_ctx* ctx, const psk_model* shard, int flags,
+                              int alg, uint64_t sengupta_n, void* elem_out);
+int psk_fold_backward(psk_ctx* ctx, int dtype, int nx, const void* elems,
+                      int count, void* info_out);
+int psk_shard_backward_finish(psk_ctx* ctx, const psk_model* shard, int flags,
+                              const void* carry_info, const void* fmean,
+                              const void* fcov, void* mean, void* cov);
 
 /* Per-kernel device time of the last call, for roofline accounting:
  * fills up to `cap` entries of names[i] (static strings) / ms[i]; returns

@@ -62,6 +62,27 @@ int main() {
     std::printf("nx=%d ny=%d alg=decoupled_lookback prts %.3e\n", d[0], d[1], ed);
     if (!(ed < 1e-9)) ++bad;
   }
+  // multi-device backends (psk_create_multi): the time axis sharded over the
+  // members, PTFS on two halves; on a one-GPU box the members are streams of
+  // GPU 0 (the exchange is then a same-device peer copy)
+  for (const std::vector<int> devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0, 0},
+                                      std::vector<int>{0, 0, 0}}) {
+    CudaBackend multi(devs);
+    const Lgssm<double> m = gen_model(31, 4, 2, 2500);
+    const Measurements<double> ys = simulate_data(m, 32);
+    for (ScanAlg alg : {kDecoupledLookback, ScanAlg::InplaceLaFi}) {
+      const ScanSpec spec{alg, 16};
+      const ScanSpec rspec{ScanAlg::InplaceLaFi, 16};
+      const double e1 = rel_err(prts_run(m, ys, spec, multi), prts_run(m, ys, rspec, pool));
+      const double e2 = rel_err(pkf_run(m, ys, spec, multi), pkf_run(m, ys, rspec, pool));
+      const double e3 = rel_err(ptfs_run(m, ys, spec, multi, multi, multi.devices()),
+                                ptfs_run(m, ys, rspec, pool, pool, 2));
+      std::printf("multi-device x%d alg=%s prts %.3e pkf %.3e ptfs(halves) %.3e\n",
+                  multi.devices(), alg == kDecoupledLookback ? "decoupled_lookback" : to_string(alg),
+                  e1, e2, e3);
+      if (!(e1 < 1e-9 && e2 < 1e-9 && e3 < 1e-9)) ++bad;
+    }
+  }
   // SoA-output overloads (caller-owned arrays) == the vector<GaussianStats> path
   {
     const Lgssm<double> m = gen_model(21, 4, 2, 3000);

@@ -17,7 +17,7 @@ PSK_E_CUDA, PSK_E_NCCL, PSK_E_ARG, PSK_E_ALLOC = 5, 6, 7, 8
 PSK_F32, PSK_F64 = 0, 1
 PSK_HOST, PSK_DEVICE = 0, 1
 PSK_MODE_FAST, PSK_MODE_EXACT = 0, 1
-PSK_SHARD_FIRST, PSK_SHARD_LAST = 1, 2
+PSK_SHARD_FIRST, PSK_SHARD_LAST, PSK_SHARD_FILTERED = 1, 2, 4
 
 
 class psk_model(C.Structure):
@@ -42,6 +42,8 @@ class psk_model(C.Structure):
 # every symbol include/psk.h declares, with its ctypes signature
 SIGNATURES = {
     "psk_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "psk_create_multi": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.c_int]),
+    "psk_num_devices": (C.c_int, [C.c_void_p]),
     "psk_destroy": (C.c_int, [C.c_void_p]),
     "psk_set_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "psk_set_chunk": (C.c_int, [C.c_void_p, C.c_int]),
@@ -67,6 +69,13 @@ SIGNATURES = {
     "psk_fold_filter": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                   C.c_void_p]),
     "psk_fold_smoother": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_void_p]),
+    "psk_shard_backward_reduce": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                            C.c_int, C.c_uint64, C.c_void_p]),
+    "psk_shard_backward_finish": (C.c_int, [C.c_void_p, C.POINTER(psk_model), C.c_int,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]),
+    "psk_fold_backward": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                     C.c_void_p]),
     "psk_set_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "psk_last_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p),

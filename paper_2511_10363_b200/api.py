@@ -158,11 +158,21 @@ class CudaBackend:
     reference's ``PoolBackend`` it must not be driven by two callers at once.
     """
 
-    def __init__(self, device: int = 0, mode: str = "fast", chunk: int = 0,
+    def __init__(self, device: Any = 0, mode: str = "fast", chunk: int = 0,
                  stream: Any = None) -> None:
+        """`device`: a CUDA device index, or a sequence of them for a
+        multi-device context (psk_create_multi: PKF / PRTS time-sharded over
+        the devices, PTFS on their two halves, batches split between them)."""
         L = _lib.lib()
         ctx = C.c_void_p()
-        _check(L.psk_create(C.byref(ctx), int(device)))
+        if isinstance(device, (list, tuple)):
+            devs = (C.c_int * len(device))(*[int(d) for d in device])
+            _check(L.psk_create_multi(C.byref(ctx), devs, len(device)))
+            self.devices = [int(d) for d in device]
+            device = self.devices[0]
+        else:
+            _check(L.psk_create(C.byref(ctx), int(device)))
+            self.devices = [int(device)]
         self._ctx = ctx
         self.device = int(device)
         self._async = False
@@ -409,6 +419,12 @@ def _ordered_call(bes: list[CudaBackend], mks: list[_Marshal], outs: list[Any], 
         return
     import torch
     cur = torch.cuda.current_stream(dev)
+    if any(len(be.devices) > 1 for be in bes):
+        # multi-device calls are synchronous and run on their members' own
+        # streams: the inputs must be complete before they start
+        cur.synchronize()
+        call()
+        return
     exts = []
     for be in bes:
         h = be.stream_handle()

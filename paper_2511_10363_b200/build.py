@@ -10,6 +10,7 @@ to the GPU box with the tree).
 from __future__ import annotations
 
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -28,16 +29,30 @@ UNITS = {
     "psk_fast_f32.cu": [],
     "psk_fast_f64.cu": [],
     "psk_exact.cu": ["--fmad=false"],
+    "psk_tile_f32.cu": [],
+    "psk_tile_f64.cu": [],
 }
+
+
+_INC = re.compile(r'^\s*#\s*include\s+"([^"]+)"', re.M)
+
+
+def _deps(src: Path, seen: set | None = None) -> set:
+    """The quoted includes of src, transitively (local headers only)."""
+    seen = set() if seen is None else seen
+    if src in seen or not src.exists():
+        return seen
+    seen.add(src)
+    for name in _INC.findall(src.read_text(errors="replace")):
+        _deps((src.parent / name).resolve(), seen)
+    return seen
 
 
 def _needs(obj: Path, src: Path) -> bool:
     if not obj.exists():
         return True
-    deps = [src] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + \
-        list(CSRC.glob("*.hpp")) + [PKG.parent / "include" / "psk.h"]
     t = obj.stat().st_mtime
-    return any(d.stat().st_mtime > t for d in deps if d.exists())
+    return any(d.stat().st_mtime > t for d in _deps(src.resolve()))
 
 
 def _compile(unit: str, extra: list[str], verbose: bool) -> tuple[str, int, str]:

@@ -40,6 +40,7 @@ struct psk_ctx {
   int mode = PSK_MODE_FAST;
   long long chunk = 0;  // 0: auto (whole waves of chunks)
   int waves = 0;        // waves of chunks for the auto chunk length (0: per precision)
+  int tile = 1;         // register-tiled kernels for their (nx, ny) (option "tile")
   int shard_async = 0;  // shard phases 0-2 and folds return without a host sync
   int async = 0;        // drivers return once queued; psk_sync reports errors
   unsigned* d_err = nullptr;
@@ -56,6 +57,9 @@ struct psk_ctx {
   int batch_streams = 4;
   std::vector<cudaStream_t> sub;
   std::vector<cudaEvent_t> sub_ev;  // fork (index 0) / join events
+  // multi-device context (psk_create_multi): one member context per device
+  // entry; the time axis is sharded over them
+  std::vector<psk_ctx*> members;
 };
 
 namespace {
@@ -138,7 +142,7 @@ cudaError_t repitch(void* dst, size_t dpitch, const void* src, size_t spitch, si
 // device arrays (time-invariant fields keep a single block, stride 0).
 template <typename S>
 int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_fuq = 0,
-                  bool force_copy = false) {
+                  bool force_copy = false, bool extra_all = false) {
   const long long T = (long long)m->t;
   const int nx = m->nx, ny = m->ny;
   Field f[7] = {{m->f, m->f_stride, (long long)nx * nx, "f"},
@@ -174,7 +178,8 @@ int prepare_model(psk_ctx* ctx, const psk_model* m, ModelView<S>& v, int extra_f
     // pack: one block if broadcast, else T blocks (plus the boundary
     // transition of a sharded run for f/u/q) at a 16-byte-rounded pitch
     const long long nblk =
-        st == 0 ? 1 : (T > 0 ? T : 1) + ((i == 0 || i == 1 || i == 2) ? extra_fuq : 0);
+        st == 0 ? 1
+                : (T > 0 ? T : 1) + ((extra_all || i == 0 || i == 1 || i == 2) ? extra_fuq : 0);
     // small dense blocks keep their dense pitch (grouped rows), the rest is
     // rounded up to whole 16-byte rows
     const size_t pb = (bb < 16 && 16 % bb == 0) ? bb : (bb + 15) / 16 * 16;
@@ -289,6 +294,7 @@ int run_typed(psk_ctx* ctx, const psk_model* m, int method, int alg,
     a.sengupta_n = sengupta_n;
     a.chunk = ctx->chunk;
     a.waves = ctx->waves;
+    a.tile = ctx->tile;
     st = wide_run<S>(L, v, a, dmean, dcov, ctx_alloc, ctx);
     if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
     if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (wide scan)");
@@ -458,29 +464,38 @@ int batch_entry(psk_ctx* ctx, const psk_model* ms, int count, int method, int al
 }
 
 // ---- time-sharded phases --------------------------------------------------
+// phases: 0 filter reduce + scan, 1 filter finish, 2 smoother reduce + scan,
+// 3 smoother finish (PRTS, or PKF with PSK_SHARD_FILTERED: phase 1 writes the
+// filtered stats); 4 backward reduce + reverse scan, 5 backward finish fused
+// with the two-filter combination (the backward half of a sharded PTFS, whose
+// forward states arrive as dense filtered stats fmean / fcov)
 template <typename S>
 int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
-                uint64_t sn, void* mean, void* cov, const void* carry, void* elem_out) {
+                uint64_t sn, void* mean, void* cov, const void* carry, void* elem_out,
+                const void* fmean = nullptr, const void* fcov = nullptr) {
   ModelView<S> v;
   const int extra = (flags & PSK_SHARD_LAST) ? 0 : 1;
-  int st = prepare_model<S>(ctx, m, v, extra);
+  const bool bwd = phase == 4 || phase == 5;
+  // the backward pass reads element a(step i+1) at slot i: a shard that does
+  // not end the series carries one extra step of every field
+  int st = prepare_model<S>(ctx, m, v, extra, false, bwd);
   if (st) return st;
   v.prior_first = (flags & PSK_SHARD_FIRST) ? 1 : 0;
   v.last_step = (flags & PSK_SHARD_LAST) ? (long long)m->t - 1 : -1;
   FastArgs a;
-  a.method = 1;
+  a.method = bwd ? 2 : ((flags & PSK_SHARD_FILTERED) ? 0 : 1);
   a.alg = alg;
   a.sengupta_n = sn;
   a.chunk = ctx->chunk;
   a.waves = ctx->waves;
-  if (phase != 0 && phase != 2) {  // finishes reuse the scan spec of the reduce
+  if (phase != 0 && phase != 2 && phase != 4) {  // finishes reuse the reduce's scan spec
     a.alg = ctx->shard_alg;
     a.sengupta_n = ctx->shard_sn;
   } else {
     ctx->shard_alg = alg;
     ctx->shard_sn = sn;
   }
-  if (phase == 0) {
+  if (phase == 0 || phase == 4) {
     ctx_free_persist(ctx);
     if (ctx->shard_scratch) {
       if (ctx->shard_dtype == PSK_F64) fast_shard_release<double>(ctx->shard_scratch);
@@ -494,7 +509,8 @@ int shard_typed(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   st = fast_shard_phase<S>(ctx->launch, v, a, phase, &ctx->shard_scratch,
                            static_cast<S*>(mean), static_cast<S*>(cov),
                            static_cast<const S*>(carry), static_cast<S*>(elem_out),
-                           ctx_alloc_persist, ctx);
+                           ctx_alloc_persist, ctx, static_cast<const S*>(fmean),
+                           static_cast<const S*>(fcov));
   if (st == 2) return fail(PSK_E_CONTRACT, "chunk scan contract violation");
   if (st == 8) return fail(PSK_E_ALLOC, "device allocation failed (shard scan)");
   if (st) return fail(PSK_E_CUDA, "shard phase failed");
@@ -524,23 +540,32 @@ int finish_call(psk_ctx* ctx, int st) {
 }
 
 int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg, uint64_t sn,
-                void* mean, void* cov, const void* carry, void* elem_out) {
+                void* mean, void* cov, const void* carry, void* elem_out,
+                const void* fmean = nullptr, const void* fcov = nullptr) {
   if (!m) return fail(PSK_E_ARG, "null model");
+  if (flags & ~(PSK_SHARD_FIRST | PSK_SHARD_LAST | PSK_SHARD_FILTERED))
+    return fail(PSK_E_ARG, "unknown shard flags");
   if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16) return fail(PSK_E_DIM, "mat dims");
   if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
   if (m->space != PSK_DEVICE) return fail(PSK_E_ARG, "sharded runs take device-space shards");
-  if (phase == 0 || phase == 2) {
+  if (phase == 0 || phase == 2 || phase == 4) {
     int st = check_contract(alg, sn, m->t);
     if (st) return st;
   }
   if (m->t == 0) return fail(PSK_E_CONTRACT, "empty shard");
   if (!mean || !cov) return fail(PSK_E_ARG, "null stats buffer");
-  if ((phase == 0 || phase == 2) && !elem_out) return fail(PSK_E_ARG, "null element output");
+  if ((phase == 0 || phase == 2 || phase == 4) && !elem_out)
+    return fail(PSK_E_ARG, "null element output");
   if (phase == 1 && !(flags & PSK_SHARD_FIRST) && !carry)
     return fail(PSK_E_ARG, "non-first shard needs the carried filtered state");
   if (phase == 3 && !(flags & PSK_SHARD_LAST) && !carry)
     return fail(PSK_E_ARG, "non-last shard needs the carried smoothed state");
+  if (phase == 5 && !(flags & PSK_SHARD_LAST) && !carry)
+    return fail(PSK_E_ARG, "non-last shard needs the carried backward information");
+  if (phase == 5 && (!fmean || !fcov))
+    return fail(PSK_E_ARG, "backward finish needs the shard's filtered stats");
   if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (!ctx->members.empty()) return fail(PSK_E_ARG, "shard phases take a single-device context");
   if (ctx->mode != PSK_MODE_FAST) return fail(PSK_E_ARG, "sharded runs use the fast path");
   const bool ok = m->dtype == PSK_F64 ? fast_supported<double>(m->nx, m->ny)
                                       : fast_supported<float>(m->nx, m->ny);
@@ -554,12 +579,17 @@ int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
   // host synchronisation (the error word accumulates and is checked by the
   // final phase), so a rank's phases and its NCCL exchanges stay queued on
   // the stream back to back; "async": no phase synchronises (psk_sync does)
-  const bool defer = (ctx->shard_async && phase != 3) || ctx->async;
-  if (!ctx->async && (!ctx->shard_async || phase == 0))
+  // the final phases (smoother finish, PKF filter finish, backward finish)
+  // synchronise and report the device errors of the whole sequence
+  const bool final_phase = phase == 3 || phase == 5 || (phase == 1 && (flags & PSK_SHARD_FILTERED));
+  const bool defer = (ctx->shard_async && !final_phase) || ctx->async;
+  if (!ctx->async && (!ctx->shard_async || phase == 0 || phase == 4))
     cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream);
   int st = m->dtype == PSK_F64
-               ? shard_typed<double>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out)
-               : shard_typed<float>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out);
+               ? shard_typed<double>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out,
+                                     fmean, fcov)
+               : shard_typed<float>(ctx, m, flags, phase, alg, sn, mean, cov, carry, elem_out,
+                                    fmean, fcov);
   if (defer) {
     ctx_free_all(ctx);
     if (st) return st;
@@ -573,9 +603,11 @@ int shard_entry(psk_ctx* ctx, const psk_model* m, int flags, int phase, int alg,
 int fold_entry(psk_ctx* ctx, int kind, int dtype, int nx, const void* elems, int count,
                void* out) {
   if (!ctx) return fail(PSK_E_ARG, "null context");
+  if (!ctx->members.empty()) return fail(PSK_E_ARG, "folds take a single-device context");
   if (dtype != PSK_F32 && dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
   if (!elems || !out || count < 1) return fail(PSK_E_ARG, "bad fold arguments");
   if (nx < 1 || nx > 4) return fail(PSK_E_DIM, "fold supports nx 1..4");
+  if (kind < 0 || kind > 2) return fail(PSK_E_ARG, "bad fold kind");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard dg(ctx->device);
   ctx->launch.stream = ctx->stream;
@@ -723,6 +755,335 @@ int ptfs_two(psk_ctx* cf, psk_ctx* cb, const psk_model* m, int alg, uint64_t sn,
   return PSK_OK;
 }
 
+
+// ---- multi-device contexts (psk_create_multi) --------------------------------
+// One host thread drives G member contexts (one per device entry; repeated
+// devices are separate streams of one GPU).  PKF / PRTS shard the time axis
+// over the members exactly like distributed.py does over processes -- reduce,
+// exchange of the shard elements, fold, finish -- with the exchange done by
+// peer copies between the members' devices (cudaMemcpyPeerAsync over NVLink /
+// NVSwitch once peer access is enabled; a plain device copy for repeated
+// devices) ordered by events, so no member ever waits on the host.  PTFS runs
+// the forward filter time-sharded on the first half of the members and the
+// backward filter time-sharded on the second half, concurrently; the forward
+// filtered stats of each shard are the only per-step data that cross devices
+// (kalman_par.hpp:207-238).  Host inputs are copied shard
+// by shard by the member that owns the shard (every GPU on its own PCIe
+// link).  Results do not depend on G beyond rounding.
+
+inline void peer_enable(int dev, int peer) {
+  if (dev == peer) return;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return;
+  }
+  DeviceGuard dg(dev);
+  if (cudaDeviceEnablePeerAccess(peer, 0) != cudaSuccess) cudaGetLastError();
+}
+
+inline long long shard_lo(long long t, int g, int G) {
+  const long long base = t / G, rem = t % G;
+  return g * base + std::min<long long>(g, rem);
+}
+
+// steps [lo, lo + n) of a model (pointers advanced by lo steps)
+psk_model model_slice(const psk_model* m, long long lo, long long n) {
+  psk_model v = *m;
+  const size_t es = m->dtype == PSK_F64 ? 8 : 4;
+  const long long nx = m->nx, ny = m->ny;
+  const void** fp[7] = {&v.f, &v.u, &v.q, &v.h, &v.d, &v.r, &v.y};
+  const int64_t st[7] = {m->f_stride, m->u_stride, m->q_stride, m->h_stride,
+                         m->d_stride, m->r_stride, m->y_stride};
+  const long long blk[7] = {nx * nx, nx, nx * nx, ny * nx, ny, ny * ny, ny};
+  for (int i = 0; i < 7; ++i) {
+    const long long s = st[i] < 0 ? blk[i] : st[i];
+    *fp[i] = static_cast<const char*>(*fp[i]) + (size_t)(lo * s) * es;
+  }
+  v.t = (uint64_t)n;
+  return v;
+}
+
+// Stage a shard on member c (device arrays; in place when the inputs already
+// live there) and describe it as a device-space psk_model.  `extra`: one more
+// step of f/u/q (or of every field with `all`) past the shard.
+template <typename S>
+int stage_shard(psk_ctx* c, const psk_model* sv, int extra, bool all, psk_model* out) {
+  bool foreign = false;
+  if (sv->space == PSK_DEVICE) {
+    const void* fields[9] = {sv->f, sv->u, sv->q, sv->h, sv->d, sv->r, sv->y, sv->prior_mean,
+                             sv->prior_cov};
+    for (const void* p : fields) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (at.type == cudaMemoryTypeDevice && at.device != c->device) foreign = true;
+    }
+  }
+  ModelView<S> v;
+  const int st = prepare_model<S>(c, sv, v, extra, foreign, all);
+  if (st) return st;
+  *out = *sv;
+  out->space = PSK_DEVICE;
+  out->f = v.f; out->u = v.u; out->q = v.q; out->h = v.h; out->d = v.d; out->r = v.r;
+  out->y = v.y;
+  out->f_stride = v.sf; out->u_stride = v.su; out->q_stride = v.sq; out->h_stride = v.sh;
+  out->d_stride = v.sd; out->r_stride = v.sr; out->y_stride = v.sy;
+  out->prior_mean = v.m0;
+  out->prior_cov = v.p0;
+  return PSK_OK;
+}
+
+struct MultiEvents {  // one event per member, recorded / waited per exchange
+  std::vector<cudaEvent_t> ev;
+  explicit MultiEvents(const std::vector<psk_ctx*>& ms) : ev(ms.size(), nullptr) {
+    for (size_t i = 0; i < ms.size(); ++i) {
+      DeviceGuard dg(ms[i]->device);
+      cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    }
+  }
+  ~MultiEvents() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+// gather the packed elements of members `from` (in order) into member c's
+// buffer `dst`, after their producers' events
+template <typename S>
+void gather_elems(psk_ctx* c, S* dst, const std::vector<psk_ctx*>& ms, const std::vector<S*>& el,
+                  MultiEvents& evs, const std::vector<int>& from, size_t es) {
+  for (size_t k = 0; k < from.size(); ++k) {
+    const int i = from[k];
+    cudaStreamWaitEvent(c->stream, evs.ev[i], 0);
+    cudaMemcpyPeerAsync(dst + k * es, c->device, el[i], ms[i]->device, es * sizeof(S), c->stream);
+  }
+}
+
+template <typename S>
+int multi_typed(psk_ctx* ctx, const psk_model* m, int method, int alg, uint64_t sn, void* mean,
+                void* cov) {
+  std::vector<psk_ctx*> ms = ctx->members;
+  const int nx = m->nx;
+  const long long T = (long long)m->t;
+  const size_t FS = 3 * nx * nx + 2 * nx, SS = 2 * nx * nx + nx, ST = nx + nx * nx;
+  const size_t es = sizeof(S);
+  int G = (int)ms.size();
+  if (method == 2) G = G / 2 * 2;  // PTFS: two halves
+  const int H = method == 2 ? G / 2 : G;  // shards
+  if ((long long)H > T) return -1;        // fewer steps than shards: one member runs it
+  MultiEvents evs(ms);
+  std::vector<psk_model> sm(G);
+  std::vector<S*> el(G, nullptr), dm(G, nullptr), dc(G, nullptr), carry(G, nullptr);
+  std::vector<long long> lo(G), n(G);
+  std::vector<int> flags(G);
+  int st = PSK_OK;
+  auto shard_of = [&](int g) { return method == 2 ? g % H : g; };
+  for (int g = 0; g < G && !st; ++g) {  // stage the shards, allocate
+    psk_ctx* c = ms[g];
+    DeviceGuard dg(c->device);
+    const int i = shard_of(g);
+    lo[g] = shard_lo(T, i, H);
+    n[g] = shard_lo(T, i + 1, H) - lo[g];
+    const bool last = i == H - 1;
+    flags[g] = (i == 0 ? PSK_SHARD_FIRST : 0) | (last ? PSK_SHARD_LAST : 0);
+    const bool bwd = method == 2 && g >= H;
+    if (method != 1 && !bwd) flags[g] |= PSK_SHARD_FILTERED;
+    const psk_model sv = model_slice(m, lo[g], n[g]);
+    st = stage_shard<S>(c, &sv, last ? 0 : 1, bwd, &sm[g]);
+    if (st) break;
+    el[g] = static_cast<S*>(ctx_alloc(es * FS * (size_t)std::max(G, 1), c));
+    dm[g] = static_cast<S*>(ctx_alloc(es * (size_t)(n[g] * nx), c));
+    dc[g] = static_cast<S*>(ctx_alloc(es * (size_t)(n[g] * nx * nx), c));
+    carry[g] = static_cast<S*>(ctx_alloc(es * (ST + 16), c));
+    if (!el[g] || !dm[g] || !dc[g] || !carry[g]) st = fail(PSK_E_ALLOC, "multi-device scratch");
+  }
+  auto phase = [&](int g, int ph, const S* cy, const S* fm, const S* fc) {
+    psk_ctx* c = ms[g];
+    DeviceGuard dg(c->device);
+    return shard_typed<S>(c, &sm[g], flags[g], ph, alg, sn, dm[g], dc[g], cy, el[g], fm, fc);
+  };
+  auto record = [&](int g) {
+    DeviceGuard dg(ms[g]->device);
+    cudaEventRecord(evs.ev[g], ms[g]->stream);
+  };
+  // ---- forward filter (members [0, H)): reduce, gather + prefix fold, finish
+  for (int g = 0; g < H && !st; ++g) {
+    st = phase(g, 0, nullptr, nullptr, nullptr);
+    record(g);
+  }
+  for (int g = 1; g < H && !st; ++g) {
+    psk_ctx* c = ms[g];
+    DeviceGuard dg(c->device);
+    std::vector<int> from;
+    for (int i = 0; i < g; ++i) from.push_back(i);
+    S* gbuf = static_cast<S*>(ctx_alloc(es * FS * (size_t)g, c));
+    if (!gbuf) st = fail(PSK_E_ALLOC, "multi-device gather");
+    if (st) break;
+    gather_elems<S>(c, gbuf, ms, el, evs, from, FS);
+    if (fast_fold<S>(c->launch, 0, nx, gbuf, g, carry[g])) st = fail(PSK_E_ARG, "fold failed");
+  }
+  for (int g = 0; g < H && !st; ++g) {
+    st = phase(g, 1, g > 0 ? carry[g] : nullptr, nullptr, nullptr);
+    record(g);
+  }
+  if (method == 1) {  // ---- RTS smoother: reduce, gather + suffix fold, finish
+    for (int g = 0; g < G && !st; ++g) {
+      st = phase(g, 2, nullptr, nullptr, nullptr);
+      record(g);
+    }
+    for (int g = 0; g < G - 1 && !st; ++g) {
+      psk_ctx* c = ms[g];
+      DeviceGuard dg(c->device);
+      std::vector<int> from;
+      for (int i = g + 1; i < G; ++i) from.push_back(i);
+      S* gbuf = static_cast<S*>(ctx_alloc(es * SS * from.size(), c));
+      if (!gbuf) st = fail(PSK_E_ALLOC, "multi-device gather");
+      if (st) break;
+      gather_elems<S>(c, gbuf, ms, el, evs, from, SS);
+      if (fast_fold<S>(c->launch, 1, nx, gbuf, (int)from.size(), carry[g]))
+        st = fail(PSK_E_ARG, "fold failed");
+    }
+    for (int g = 0; g < G && !st; ++g)
+      st = phase(g, 3, g < G - 1 ? carry[g] : nullptr, nullptr, nullptr);
+  } else if (method == 2) {  // ---- backward filter on members [H, 2H)
+    for (int g = H; g < G && !st; ++g) {
+      st = phase(g, 4, nullptr, nullptr, nullptr);
+      record(g);
+    }
+    for (int g = H; g < G && !st; ++g) {
+      psk_ctx* c = ms[g];
+      DeviceGuard dg(c->device);
+      std::vector<int> from;
+      for (int i = g + 1; i < G; ++i) from.push_back(i);
+      if (!from.empty()) {
+        S* gbuf = static_cast<S*>(ctx_alloc(es * FS * from.size(), c));
+        if (!gbuf) st = fail(PSK_E_ALLOC, "multi-device gather");
+        if (st) break;
+        gather_elems<S>(c, gbuf, ms, el, evs, from, FS);
+        if (fast_fold<S>(c->launch, 2, nx, gbuf, (int)from.size(), carry[g]))
+          st = fail(PSK_E_ARG, "fold failed");
+      }
+      // the forward half's filtered stats of this shard
+      const int f = g - H;
+      S* fm = static_cast<S*>(ctx_alloc(es * (size_t)(n[g] * nx), c));
+      S* fc = static_cast<S*>(ctx_alloc(es * (size_t)(n[g] * nx * nx), c));
+      if (!fm || !fc) st = fail(PSK_E_ALLOC, "multi-device forward states");
+      if (st) break;
+      cudaStreamWaitEvent(c->stream, evs.ev[f], 0);
+      cudaMemcpyPeerAsync(fm, c->device, dm[f], ms[f]->device, es * (size_t)(n[g] * nx),
+                          c->stream);
+      cudaMemcpyPeerAsync(fc, c->device, dc[f], ms[f]->device, es * (size_t)(n[g] * nx * nx),
+                          c->stream);
+      c->launch.count("ptfs_forward_states_peer_copy");
+      st = phase(g, 5, from.empty() ? nullptr : carry[g], fm, fc);
+    }
+  }
+  // ---- outputs: every shard's stats into the caller's buffer (any memory)
+  const int o0 = method == 2 ? H : 0;
+  for (int g = o0; g < o0 + H && !st; ++g) {
+    psk_ctx* c = ms[g];
+    DeviceGuard dg(c->device);
+    cudaMemcpyAsync(static_cast<char*>(mean) + es * (size_t)(lo[g] * nx), dm[g],
+                    es * (size_t)(n[g] * nx), cudaMemcpyDefault, c->stream);
+    cudaMemcpyAsync(static_cast<char*>(cov) + es * (size_t)(lo[g] * nx * nx), dc[g],
+                    es * (size_t)(n[g] * nx * nx), cudaMemcpyDefault, c->stream);
+  }
+  return st;
+}
+
+int multi_entry(psk_ctx* ctx, const psk_model* m, int method, int alg, uint64_t sn, void* mean,
+                void* cov) {
+  if (!m) return fail(PSK_E_ARG, "null model");
+  if (m->nx < 1 || m->nx > 16 || m->ny < 1 || m->ny > 16) return fail(PSK_E_DIM, "mat dims");
+  if (m->dtype != PSK_F32 && m->dtype != PSK_F64) return fail(PSK_E_ARG, "bad dtype");
+  if (m->space != PSK_HOST && m->space != PSK_DEVICE) return fail(PSK_E_ARG, "bad space");
+  int st = check_contract(alg, sn, m->t);
+  if (st) return st;
+  if (m->t > 0 && (!mean || !cov)) return fail(PSK_E_ARG, "null output");
+  std::vector<psk_ctx*> ms = ctx->members;
+  const bool fast = ctx->mode == PSK_MODE_FAST &&
+                    (m->dtype == PSK_F64 ? fast_supported<double>(m->nx, m->ny)
+                                         : fast_supported<float>(m->nx, m->ny));
+  const int G = (int)ms.size();
+  if (!fast || G < 2 || (method == 2 && G < 2) || m->t < 2) {
+    // a single member runs it (dims without shard phases, exact mode, tiny
+    // series): the numbers do not depend on the placement
+    if (method == 2) return psk_ptfs(ms[0], ms[0], 1, m, alg, sn, mean, cov);
+    return run_entry(ms[0], m, method, alg, sn, mean, cov);
+  }
+  std::lock_guard<std::mutex> lk0(ctx->mu);
+  std::vector<psk_ctx*> order = ms;  // lock members in address order
+  std::sort(order.begin(), order.end());
+  order.erase(std::unique(order.begin(), order.end()), order.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (psk_ctx* c : order) locks.emplace_back(c->mu);
+  for (psk_ctx* c : order) {
+    DeviceGuard dg(c->device);
+    c->launch.stream = c->stream;
+    c->launch.err = c->d_err;
+    c->launch.start();
+    cudaMemsetAsync(c->d_err, 0, sizeof(unsigned), c->stream);
+  }
+  st = m->dtype == PSK_F64 ? multi_typed<double>(ctx, m, method, alg, sn, mean, cov)
+                           : multi_typed<float>(ctx, m, method, alg, sn, mean, cov);
+  if (st == -1) {  // fewer steps than shards
+    locks.clear();
+    if (method == 2) return psk_ptfs(ms[0], ms[0], 1, m, alg, sn, mean, cov);
+    return run_entry(ms[0], m, method, alg, sn, mean, cov);
+  }
+  unsigned herr_all = 0;
+  cudaError_t e = cudaSuccess;
+  long long launches = 0;
+  std::vector<unsigned> herr(order.size(), 0);
+  for (size_t i = 0; i < order.size(); ++i) {
+    psk_ctx* c = order[i];
+    DeviceGuard dg(c->device);
+    cudaMemcpyAsync(&herr[i], c->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream);
+    ctx_free_all(c);
+  }
+  for (size_t i = 0; i < order.size(); ++i) {
+    psk_ctx* c = order[i];
+    DeviceGuard dg(c->device);
+    const cudaError_t ec = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = ec;
+    herr_all |= herr[i];
+    launches += c->launch.launches;
+  }
+  ctx->launch.launches = launches;
+  if (st) return st;
+  if (e != cudaSuccess) return fail(PSK_E_CUDA, std::string("execution: ") + cuda_msg(e));
+  if (herr_all & kErrNotPD) return fail(PSK_E_NOT_PD, "cholesky pivot");
+  if (herr_all & kErrSingular) return fail(PSK_E_SINGULAR, "lu zero pivot");
+  return PSK_OK;
+}
+
+// A batch on a multi-device context: contiguous shares of the series per
+// member (BASELINE configs[4] batch sharding, no exchange), all members
+// queued before any waits.
+int multi_batch_entry(psk_ctx* ctx, const psk_model* ms_, int count, int method, int alg,
+                      uint64_t sn, void* const* means, void* const* covs) {
+  std::vector<psk_ctx*> ms = ctx->members;
+  const int G = (int)ms.size();
+  std::vector<int> was(G);
+  int st = PSK_OK;
+  for (int g = 0; g < G && !st; ++g) {
+    const long long a = shard_lo(count, g, G), b = shard_lo(count, g + 1, G);
+    if (b == a) continue;
+    was[g] = ms[g]->async;
+    ms[g]->async = 1;
+    st = batch_entry(ms[g], ms_ + a, (int)(b - a), method, alg, sn, means + a, covs + a);
+    ms[g]->async = was[g];
+  }
+  int st2 = PSK_OK;
+  for (int g = 0; g < G; ++g) {
+    const int s2 = psk_sync(ms[g]);
+    if (!st2) st2 = s2;
+  }
+  return st ? st : st2;
+}
 }  // namespace
 
 extern "C" {
@@ -754,8 +1115,39 @@ int psk_create(psk_ctx** out, int device) {
   return PSK_OK;
 }
 
+int psk_create_multi(psk_ctx** out, const int* devices, int ndev) {
+  if (!out) return fail(PSK_E_ARG, "null ctx out");
+  *out = nullptr;
+  if (!devices || ndev < 1 || ndev > 64) return fail(PSK_E_ARG, "devices: 1..64 entries");
+  std::vector<psk_ctx*> ms;
+  for (int i = 0; i < ndev; ++i) {
+    psk_ctx* c = nullptr;
+    const int st = psk_create(&c, devices[i]);
+    if (st) {
+      for (psk_ctx* x : ms) psk_destroy(x);
+      return st;
+    }
+    ms.push_back(c);
+  }
+  for (int i = 0; i < ndev; ++i)  // NVLink P2P between every pair of members
+    for (int j = 0; j < ndev; ++j) peer_enable(devices[i], devices[j]);
+  auto* c = new psk_ctx;
+  c->device = devices[0];
+  c->own_stream = nullptr;
+  c->stream = ms[0]->stream;
+  c->d_err = nullptr;
+  c->members = std::move(ms);
+  *out = c;
+  return PSK_OK;
+}
+
 int psk_destroy(psk_ctx* c) {
   if (!c) return PSK_OK;
+  if (!c->members.empty()) {
+    for (psk_ctx* m : c->members) psk_destroy(m);
+    delete c;
+    return PSK_OK;
+  }
   {
     DeviceGuard dg(c->device);
     ctx_free_persist(c);
@@ -779,6 +1171,7 @@ int psk_set_mode(psk_ctx* c, int mode) {
   if (!c) return fail(PSK_E_ARG, "null context");
   if (mode != PSK_MODE_FAST && mode != PSK_MODE_EXACT) return fail(PSK_E_ARG, "bad mode");
   c->mode = mode;
+  for (psk_ctx* m : c->members) m->mode = mode;
   return PSK_OK;
 }
 
@@ -786,11 +1179,23 @@ int psk_set_chunk(psk_ctx* c, int chunk) {
   if (!c) return fail(PSK_E_ARG, "null context");
   if (chunk < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
   c->chunk = chunk;
+  for (psk_ctx* m : c->members) m->chunk = chunk;
   return PSK_OK;
 }
 
 int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(PSK_E_ARG, "null context or key");
+  if (!c->members.empty()) {  // a multi-device context: every member
+    const std::string k(key);
+    if (k == "async" || k == "shard_async")
+      return fail(PSK_E_ARG, "multi-device calls are synchronous");
+    for (psk_ctx* m : c->members) {
+      const int st = psk_set_option(m, key, value);
+      if (st) return st;
+    }
+    if (k == "chunk") c->chunk = value;
+    return PSK_OK;
+  }
   const std::string k(key);
   if (k == "chunk") {
     if (value < 0) return fail(PSK_E_ARG, "chunk must be >= 1 (or 0 = auto)");
@@ -823,6 +1228,9 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
       c->launch.dlb_trace = nullptr;
       c->launch.dlb_trace_cap = 0;
     }
+  } else if (k == "tile") {
+    if (value != 0 && value != 1) return fail(PSK_E_ARG, "tile must be 0 or 1");
+    c->tile = (int)value;
   } else if (k == "waves") {
     if (value < 1 || value > 1024) return fail(PSK_E_ARG, "waves must be 1..1024");
     c->waves = (int)value;
@@ -834,6 +1242,14 @@ int psk_set_option(psk_ctx* c, const char* key, int64_t value) {
 
 int psk_sync(psk_ctx* c) {
   if (!c) return fail(PSK_E_ARG, "null context");
+  if (!c->members.empty()) {
+    int st = PSK_OK;
+    for (psk_ctx* m : c->members) {
+      const int s2 = psk_sync(m);
+      if (!st) st = s2;
+    }
+    return st;
+  }
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard dg(c->device);
   unsigned herr = 0;
@@ -863,6 +1279,7 @@ int psk_sync(psk_ctx* c) {
 
 int psk_set_stream(psk_ctx* c, void* stream) {
   if (!c) return fail(PSK_E_ARG, "null context");
+  if (!c->members.empty()) return fail(PSK_E_ARG, "a multi-device context runs on its members' streams");
   c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
   return PSK_OK;
 }
@@ -892,13 +1309,22 @@ int psk_last_profile(psk_ctx* c, const char** names, float* ms, int cap) {
 int64_t psk_last_launch_count(psk_ctx* c) { return c ? c->launch.launches : -1; }
 
 int psk_pkf(psk_ctx* c, const psk_model* m, int alg, uint64_t sn, void* mean, void* cov) {
+  if (c && !c->members.empty()) return multi_entry(c, m, 0, alg, sn, mean, cov);
   return run_entry(c, m, 0, alg, sn, mean, cov);
 }
 int psk_prts(psk_ctx* c, const psk_model* m, int alg, uint64_t sn, void* mean, void* cov) {
+  if (c && !c->members.empty()) return multi_entry(c, m, 1, alg, sn, mean, cov);
   return run_entry(c, m, 1, alg, sn, mean, cov);
 }
 int psk_ptfs(psk_ctx* cf, psk_ctx* cb, int devices, const psk_model* m, int alg, uint64_t sn,
              void* mean, void* cov) {
+  if (cf && !cf->members.empty()) {
+    // a multi-device forward context: the two filters on its member halves
+    // (devices = 1 keeps the whole smoother on the first member)
+    if (devices == 1) return psk_ptfs(cf->members[0], cf->members[0], 1, m, alg, sn, mean, cov);
+    return multi_entry(cf, m, 2, alg, sn, mean, cov);
+  }
+  if (cb && !cb->members.empty()) return fail(PSK_E_ARG, "multi-device backward context");
   if (devices != 1 && devices != 2) return fail(PSK_E_ARG, "devices must be 1 or 2");
   if (!cb) cb = cf;
   // devices == 2 with a second context: forward filter on ctx_fwd and the
@@ -932,6 +1358,17 @@ int psk_shard_smoother_finish(psk_ctx* c, const psk_model* m, int flags, const v
                               void* mean, void* cov) {
   return shard_entry(c, m, flags, 3, 0, 1, mean, cov, carry, nullptr);
 }
+int psk_shard_backward_reduce(psk_ctx* c, const psk_model* m, int flags, int alg, uint64_t sn,
+                              void* elem_out) {
+  return shard_entry(c, m, flags, 4, alg, sn, elem_out, elem_out, nullptr, elem_out);
+}
+int psk_shard_backward_finish(psk_ctx* c, const psk_model* m, int flags, const void* carry,
+                              const void* fmean, const void* fcov, void* mean, void* cov) {
+  return shard_entry(c, m, flags, 5, 0, 1, mean, cov, carry, nullptr, fmean, fcov);
+}
+int psk_fold_backward(psk_ctx* c, int dtype, int nx, const void* elems, int count, void* out) {
+  return fold_entry(c, 2, dtype, nx, elems, count, out);
+}
 int psk_fold_filter(psk_ctx* c, int dtype, int nx, const void* elems, int count, void* out) {
   return fold_entry(c, 0, dtype, nx, elems, count, out);
 }
@@ -941,11 +1378,18 @@ int psk_fold_smoother(psk_ctx* c, int dtype, int nx, const void* elems, int coun
 
 int psk_pkf_batch(psk_ctx* c, const psk_model* ms, int count, int alg, uint64_t sn,
                   void* const* means, void* const* covs) {
+  if (c && !c->members.empty()) return multi_batch_entry(c, ms, count, 0, alg, sn, means, covs);
   return batch_entry(c, ms, count, 0, alg, sn, means, covs);
 }
 int psk_prts_batch(psk_ctx* c, const psk_model* ms, int count, int alg, uint64_t sn,
                    void* const* means, void* const* covs) {
+  if (c && !c->members.empty()) return multi_batch_entry(c, ms, count, 1, alg, sn, means, covs);
   return batch_entry(c, ms, count, 1, alg, sn, means, covs);
+}
+
+int psk_num_devices(psk_ctx* c) {
+  if (!c) return fail(PSK_E_ARG, "null context");
+  return c->members.empty() ? 1 : (int)c->members.size();
 }
 
 int psk_host_alloc(void** p, size_t bytes) {

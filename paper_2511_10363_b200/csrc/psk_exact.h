@@ -113,6 +113,7 @@ struct FastArgs {
   unsigned long long sengupta_n = 1;
   long long chunk = 32;
   int waves = 0;        // auto chunk (chunk = 0): whole waves of chunks (0: default)
+  int tile = 1;         // dims > 4: register-tiled kernels where instantiated (psk_tile*.cuh)
 };
 template <typename S>
 bool fast_supported(int nx, int ny);
@@ -126,6 +127,12 @@ template <typename S>
 int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
              void* (*alloc)(size_t, void*), void* alloc_ctx);
 
+// register-tiled warp kernels for compile-time (nx, ny) (psk_tile_impl.cuh);
+// -1 when the request has no instantiation (then the wide path runs)
+template <typename S>
+int tile_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
+             void* (*alloc)(size_t, void*), void* alloc_ctx);
+
 // PTFS with forward (A) and backward (B) passes on two contexts
 template <typename S>
 int fast_ptfs2(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& LB,
@@ -136,7 +143,8 @@ int fast_ptfs2(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& L
 template <typename S>
 int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
                      void** scratch, S* mean, S* cov, const S* carry, S* elem_out,
-                     void* (*alloc)(size_t, void*), void* actx);
+                     void* (*alloc)(size_t, void*), void* actx, const S* fmean = nullptr,
+                     const S* fcov = nullptr);
 template <typename S>
 void fast_shard_release(void* scratch);
 template <typename S>

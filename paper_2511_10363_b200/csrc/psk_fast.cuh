@@ -939,11 +939,31 @@ __global__ void __launch_bounds__(kSmoothNT)
 // step i+1) or the identity (build_shifted_filter_elems, kalman_par.hpp:
 // 63-89); `ms` is the model shifted by one step (ms step i = m step i+1,
 // ms.t = T - 1), staged by TMA like the forward passes.
+// (eta, J) <- the eta / J rows of a (x) (., ., ., eta, J) (Lemma 1,
+// kalman_elems.hpp:267-336: they depend on the right operand through its
+// (eta, J) alone): N = I + J C_a, eta' = A_a^T N^-1 (eta - J b_a) + eta_a,
+// J' = A_a^T N^-1 J A_a + J_a
+template <typename S, int NX>
+__device__ __forceinline__ void bwd_info_apply(const FElem<S, NX>& a, Vec<S, NX>& eta,
+                                               Mat<S, NX, NX>& J, unsigned& e) {
+  Mat<S, NX, NX> nm = mul(J, a.C);
+#pragma unroll
+  for (int q = 0; q < NX; ++q) nm.a[q][q] += S(1);
+  const LU<S, NX> lu = lu_factor(nm, e);
+  const Vec<S, NX> w = sub_mul(eta, J, a.b);
+  const Vec<S, NX> y = lu_solve(lu, w);
+  const Mat<S, NX, NX> yj = lu_solve(lu, J);
+  const Mat<S, NX, NX> v = mul(yj, a.A);
+  eta = mul_tn_add(a.A, y, a.eta);
+  J = mul_tn_sym_add(a.A, v, a.J);
+}
+
 template <typename S, int NX, int NY>
 __global__ void __launch_bounds__(kStageNT, 2)
     k_bwd_finish(ModelView<S> ms, const __grid_constant__ StageMaps maps, long long T,
                  long long L, long long nchunks, long long nfull, const S* suf, long long suf_cap,
-                 ChunkOrder bord, const S* fst, long long fcap, S* mean, S* cov, unsigned* err) {
+                 ChunkOrder bord, const S* fst, long long fcap, S* mean, S* cov,
+                 const S* carry, const S* fmean, const S* fcov, unsigned* err) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   using St = FilterStage<S, NX, NY>;
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -955,7 +975,17 @@ __global__ void __launch_bounds__(kStageNT, 2)
   const long long jn = min(L, T - cta0 * L);  // CTA-uniform (slots of the CTA's first chunk)
   Vec<S, NX> eta = zeros<S, NX, 1>();
   Mat<S, NX, NX> J = zeros<S, NX, NX>();
-  if (live && c + 1 < nchunks) {
+  if (live && carry != nullptr) {
+    // time-sharded backward pass: (eta, J) of the later shards' backward
+    // elements folded (the backward information of everything after this
+    // shard); the shard's own suffix of chunk c+1 is applied on top of it
+    eta = load_soa<S, NX, 1>(carry, 1);
+    J = load_soa<S, NX, NX>(carry + NX, 1);
+    if (c + 1 < nchunks) {
+      const FElem<S, NX> a = fe_load<S, NX>(suf, suf_cap, bord.at(c + 1));
+      bwd_info_apply(a, eta, J, e);
+    }
+  } else if (live && c + 1 < nchunks) {
     const long long q = bord.at(c + 1);
     eta = load_soa<S, NX, 1>(suf + FLayout<NX>::eta * suf_cap + q, suf_cap);
     J = load_soa<S, NX, NX>(suf + FLayout<NX>::J * suf_cap + q, suf_cap);
@@ -971,21 +1001,17 @@ __global__ void __launch_bounds__(kStageNT, 2)
       a.b = in.u();
       a.C = in.Q();
       cond_update(a, in.meas(), e);
-      Mat<S, NX, NX> nm = mul(J, a.C);  // N = I + J_s C_a
-#pragma unroll
-      for (int q = 0; q < NX; ++q) nm.a[q][q] += S(1);
-      const LU<S, NX> lu = lu_factor(nm, e);
-      const Vec<S, NX> w = sub_mul(eta, J, a.b);
-      const Vec<S, NX> y = lu_solve(lu, w);
-      const Mat<S, NX, NX> yj = lu_solve(lu, J);
-      const Mat<S, NX, NX> v = mul(yj, a.A);
-      eta = mul_tn_add(a.A, y, a.eta);
-      J = mul_tn_sym_add(a.A, v, a.J);
+      bwd_info_apply(a, eta, J, e);
     }
     // two-filter combination: (I + P J)^-1 (x + P eta), (I + P J)^-1 P
     Vec<S, NX> x;
     Mat<S, NX, NX> P;
-    state_load(fst + (i - k0) * StateLayout<NX>::size * fcap + c, fcap, x, P);
+    if (fmean != nullptr) {  // dense forward states of another device's forward pass
+      x = load<S, NX, 1>(fmean + i * NX);
+      P = load<S, NX, NX>(fcov + i * NX * NX);
+    } else {
+      state_load(fst + (i - k0) * StateLayout<NX>::size * fcap + c, fcap, x, P);
+    }
     Mat<S, NX, NX> mm = mul(P, J);
 #pragma unroll
     for (int q = 0; q < NX; ++q) mm.a[q][q] += S(1);
@@ -1019,6 +1045,20 @@ __global__ void k_fold_filter(const S* aggs, int count, S* out, unsigned* err) {
   for (int i = 0; i < NX; ++i) out[i] = acc.b.a[i][0];
   for (int i = 0; i < NX; ++i)
     for (int j = 0; j < NX; ++j) out[NX + i * NX + j] = acc.C.a[i][j];
+  if (e) atomicOr(err, e);
+}
+// Fold of `count` packed backward (shifted filter) elements, left to right:
+// the backward information (eta | J) of the later shards of a sharded PTFS.
+template <typename S, int NX>
+__global__ void k_fold_backward(const S* aggs, int count, S* out, unsigned* err) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned e = 0;
+  constexpr int FS = FLayout<NX>::size;
+  FElem<S, NX> acc = fe_load<S, NX>(aggs, 1, 0);
+  for (int k = 1; k < count; ++k) acc = filter_combine(acc, fe_load<S, NX>(aggs + k * FS, 1, 0), e);
+  for (int i = 0; i < NX; ++i) out[i] = acc.eta.a[i][0];
+  for (int i = 0; i < NX; ++i)
+    for (int j = 0; j < NX; ++j) out[NX + i * NX + j] = acc.J.a[i][j];
   if (e) atomicOr(err, e);
 }
 // Fold of `count` packed smoother elements, left to right; the last contains

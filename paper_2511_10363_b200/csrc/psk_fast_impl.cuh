@@ -53,7 +53,9 @@ ModelView<S> shift_model(const ModelView<S>& m) {
   v.d += m.sd;
   v.r += m.sr;
   v.y += m.sy;
-  v.t = m.t > 0 ? m.t - 1 : 0;
+  // a time shard that does not end the series carries one extra step of
+  // every field (last_step < 0), so its shifted view keeps all t slots
+  v.t = m.last_step < 0 ? m.t : (m.t > 0 ? m.t - 1 : 0);
   v.prior_first = 0;
   v.last_step = v.t - 1;
   return v;
@@ -223,6 +225,10 @@ struct FastScratch {
   long long ecap = 0;       // chunk capacity of egl (a multiple of 32: TMA rows)
   bool sagg_valid = false;
   void* dlb = nullptr;
+  // sharded PTFS backward finish: the forward half's filtered stats of this
+  // shard (dense mean[t][nx], cov[t][nx][nx]) in place of egl
+  const S* fmean = nullptr;
+  const S* fcov = nullptr;
 };
 
 template <typename S, int NX, int NY>
@@ -388,6 +394,11 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
         L.count("fill_identity");
       }
       chunk_scan(L, fops, a, sc.agg, nch, npad, 1, sc.aux1, sc.aux2, sc.plan, sc.dlb, sc.cap);
+      if (elem_out) {  // the shard's backward total (reverse scan value of chunk 0)
+        k_extract_elem<<<1, 64, 0, L.stream>>>(sc.agg, sc.cap, sc.bord.at(0),
+                                               FLayout<NX>::size, elem_out);
+        L.count("extract_elem");
+      }
       break;
     }
     case 5: {
@@ -398,7 +409,7 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       kernel_setup(k_bwd_finish<S, NX, NY>, kStageNT, stage_bytes);
       k_bwd_finish<S, NX, NY><<<gs, kStageNT, stage_bytes, L.stream>>>(
           ms, smaps, m.t, Lc, nch, ms.t / Lc, sc.agg, sc.cap, sc.bord, sc.egl, sc.ecap, mean,
-          cov, L.err);
+          cov, carry, sc.fmean, sc.fcov, L.err);
       L.count("bwd_finish_tf_combine");
       break;
     }
@@ -521,18 +532,23 @@ int fast_ptfs2(ExactLaunch& LA, const ModelView<S>& mA, int devA, ExactLaunch& L
 
 // one phase of a sharded run; `scratch` is an opaque FastScratch<S> owned by
 // the caller (allocated on phase 0 / 2 with the persistent allocator)
+// phase 5 (sharded PTFS backward finish) reads the forward states from the
+// dense (fmean, fcov) arrays instead of the scratch the forward finish fills.
 template <typename S>
 int fast_shard_phase(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, int phase,
                      void** scratch, S* mean, S* cov, const S* carry, S* elem_out,
-                     void* (*alloc)(size_t, void*), void* actx) {
+                     void* (*alloc)(size_t, void*), void* actx, const S* fmean,
+                     const S* fcov) {
   auto* sc = static_cast<FastScratch<S>*>(*scratch);
   if (!sc) {
     sc = new FastScratch<S>();
     *scratch = sc;
   }
+  sc->fmean = fmean;
+  sc->fcov = fcov;
 #define PSK_CASE(A, B)                                                           \
   if (m.nx == A && m.ny == B) {                                                  \
-    if (phase == 0) {                                                            \
+    if (phase == 0 || phase == 4) {                                              \
       int st = fast_prepare_t<S, A, B>(m, a, *sc, alloc, actx);                    \
       if (st) return st;                                                         \
     }                                                                            \
@@ -555,9 +571,11 @@ int fast_fold(ExactLaunch& L, int kind, int nx, const S* aggs, int count, S* out
   if (nx == N) {                                                               \
     if (kind == 0)                                                             \
       k_fold_filter<S, N><<<1, 32, 0, L.stream>>>(aggs, count, out, L.err);    \
-    else                                                                       \
+    else if (kind == 1)                                                        \
       k_fold_smoother<S, N><<<1, 32, 0, L.stream>>>(aggs, count, out);         \
-    L.count(kind == 0 ? "fold_filter" : "fold_smoother");                      \
+    else                                                                       \
+      k_fold_backward<S, N><<<1, 32, 0, L.stream>>>(aggs, count, out, L.err);  \
+    L.count(kind == 0 ? "fold_filter" : kind == 1 ? "fold_smoother" : "fold_backward"); \
     return 0;                                                                  \
   }
   PSK_FOLD(1) PSK_FOLD(2) PSK_FOLD(3) PSK_FOLD(4)

@@ -97,11 +97,28 @@ class CudaShardEngine:
                                                     self.flags, self._p(carry), self._p(mean),
                                                     self._p(cov)))
 
+    def backward_reduce(self, spec):
+        """PTFS backward half: shifted elements of the shard + reverse scan;
+        returns the shard's backward total (a filter element)."""
+        from .api import _check
+        out = self.empty(3 * self.nx * self.nx + 2 * self.nx)
+        _check(_lib.lib().psk_shard_backward_reduce(self.be.handle, C.byref(self.mk.model),
+                                                    self.flags, int(spec.alg),
+                                                    int(spec.sengupta_n), self._p(out)))
+        return out
+
+    def backward_finish(self, carry, fmean, fcov, mean, cov):
+        from .api import _check
+        _check(_lib.lib().psk_shard_backward_finish(self.be.handle, C.byref(self.mk.model),
+                                                    self.flags, self._p(carry), self._p(fmean),
+                                                    self._p(fcov), self._p(mean), self._p(cov)))
+
     def fold(self, kind: str, elems):
         from .api import _check
         st = self.empty(self.nx + self.nx * self.nx)
         stacked = self.torch.stack(list(elems)).contiguous()
-        fn = _lib.lib().psk_fold_filter if kind == "filter" else _lib.lib().psk_fold_smoother
+        fn = {"filter": _lib.lib().psk_fold_filter, "smoother": _lib.lib().psk_fold_smoother,
+              "backward": _lib.lib().psk_fold_backward}[kind]
         _check(fn(self.be.handle, _lib.PSK_F64 if self.mk.f64 else _lib.PSK_F32, self.nx,
                   self._p(stacked), len(elems), self._p(st)))
         return st
@@ -161,6 +178,102 @@ def shard_model(model, ys, lo: int, hi: int, device: Any = None, dtype: Any = No
               t=hi_in - lo)
     y = ys if isinstance(ys, torch.Tensor) else torch.as_tensor(np.asarray(ys))
     return m, put(y[lo:hi_in])
+
+
+def ptfs_halves(rank: int, world: int) -> tuple[bool, int, int]:
+    """(forward?, shard index, shards per half) of a rank of the sharded PTFS:
+    ranks [0, G/2) run the forward filter, [G/2, G) the backward filter, rank
+    r and r + G/2 own the same step range (PAPER.md:883-892 with each half
+    time-sharded)."""
+    if world < 2 or world % 2:
+        raise ValueError("the two-filter smoother splits an even number of ranks in halves")
+    h = world // 2
+    return rank < h, rank % h, h
+
+
+def ptfs_groups(world: int):
+    """The two half groups (every rank must create both, in this order)."""
+    import torch.distributed as dist
+    h = world // 2
+    return dist.new_group(list(range(h))), dist.new_group(list(range(h, world)))
+
+
+def ptfs_sharded(engine, spec, rank: int, world: int, t_shard: int, groups=None):
+    """The parallel two-filter smoother (Alg. 7, kalman_par.hpp:207-238) on
+    disjoint GPU halves, each half time-sharded:
+
+      forward rank i:   sharded PKF of shard i (all_gather of shard elements in
+                        the forward group, prefix fold, finish) -> filtered
+                        stats, sent to backward rank h + i (20 scalars / step
+                        at nx = 4: the only per-step data that crosses GPUs);
+      backward rank i:  shifted elements + reverse scan of shard i,
+                        all_gather of the shard totals in the backward group,
+                        fold of the LATER shards -> (eta, J) carry, then the
+                        backward finish fused with the two-filter combination
+                        over the received filtered stats -> smoothed stats.
+
+    The two halves run concurrently.  Returns the smoothed (mean, cov) of the
+    shard on backward ranks, None on forward ranks.  `engine` is a
+    CudaShardEngine (forward ranks built with PSK_SHARD_FILTERED) or a test
+    double with the same methods."""
+    import torch.distributed as dist
+
+    fwd, i, h = ptfs_halves(rank, world)
+    gf, gb = groups if groups is not None else (None, None)
+    if fwd:
+        a = engine.filter_reduce(spec)
+        gathered = all_gather(a, h, gf) if h > 1 else [a]
+        carry = engine.fold("filter", gathered[:i]) if i > 0 else None
+        mean, cov = engine.stats(t_shard)
+        engine.filter_finish(carry, mean, cov)
+        _p2p(dist.send, mean, h + i)
+        _p2p(dist.send, cov, h + i)
+        return None
+    s = engine.backward_reduce(spec)
+    gathered = all_gather(s, h, gb) if h > 1 else [s]
+    carry = engine.fold("backward", gathered[i + 1:]) if i < h - 1 else None
+    fmean, fcov = engine.stats(t_shard)
+    _p2p(dist.recv, fmean, i)
+    _p2p(dist.recv, fcov, i)
+    mean, cov = engine.stats(t_shard)
+    engine.backward_finish(carry, fmean, fcov, mean, cov)
+    return mean, cov
+
+
+def _p2p(op, t, peer: int) -> None:
+    """Point-to-point send / recv of `t`: NCCL moves device tensors directly
+    (NVLink); gloo (the CPU test rig) only moves host tensors, so a device
+    tensor is staged through host memory there."""
+    import torch.distributed as dist
+    if dist.get_backend() == "gloo" and getattr(t, "is_cuda", False):
+        h = t.cpu()
+        op(h, peer)
+        if op is dist.recv:
+            t.copy_(h)
+        return
+    op(t, peer)
+
+
+def ptfs_flags(rank: int, world: int) -> int:
+    """Shard flags of a sharded-PTFS rank (its half's shard position)."""
+    fwd, i, h = ptfs_halves(rank, world)
+    f = shard_flags(i, h)
+    return f | (_lib.PSK_SHARD_FILTERED if fwd else 0)
+
+
+def ptfs_run_sharded(model, ys, spec, be, rank: int, world: int, lo: int, hi: int,
+                     groups=None, engine: Any = None):
+    """PTFS over shard [lo, hi) (shard_range(T, rank % (world/2), world/2)) on
+    one rank of the two halves; `model`/`ys` hold the shard's steps plus one
+    extra step of every field unless hi == T (shard_model).  Returns the
+    smoothed GaussianStats of the shard on backward ranks, None on forward
+    ranks."""
+    from . import api
+
+    if engine is None:
+        engine = CudaShardEngine(be, model, ys, ptfs_flags(rank, world), hi - lo)
+    out = ptfs_sharded(engine, spec, rank, world, hi - lo, groups)
+    return None if out is None else api.GaussianStats(*out)
 
 
 def shard_flags(rank: int, world: int) -> int:

@@ -79,3 +79,101 @@ def test_prts_run_sharded_processes(gpu, tmp_path, rts_ref, world, alg):
         e = max_rel_err(d["mean"], d["cov"], rm[lo:hi], rc[lo:hi])
         assert e < 1e-9, (r, e)
     assert covered == T
+
+
+def _batch_worker(rank, world, port, out_dir):
+    """BASELINE configs[4]'s multi-GPU form: batch sharding, no exchange --
+    each rank runs its contiguous share of the series through one
+    psk_prts_batch call (distributed.prts_run_batch_sharded)."""
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200 import distributed as dp
+    from oracle.oracle import Oracle
+    from test_gpu_headline import _config5_series
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle("port")
+    series = [_config5_series(orc, psk, b, 2048) for b in range(5)]
+    be = psk.CudaBackend(0)
+    idx, res = dp.prts_run_batch_sharded([s[0] for s in series], [s[1] for s in series],
+                                         psk.ScanSpec(psk.ScanAlg.DecoupledLookback), be,
+                                         rank, world)
+    np.savez(Path(out_dir) / f"b{rank}.npz", idx=np.array(list(idx)),
+             **{f"m{i}": r.mean for i, r in zip(idx, res)},
+             **{f"c{i}": r.cov for i, r in zip(idx, res)})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_config5_batch_sharded_processes(gpu, tmp_path, port):
+    import torch.multiprocessing as mp
+
+    import paper_2511_10363_b200 as psk
+    from test_gpu_headline import _config5_series
+
+    world = 2
+    mp.spawn(_batch_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    seen = []
+    for r in range(world):
+        d = np.load(tmp_path / f"b{r}.npz")
+        for i in d["idx"]:
+            m, ys = _config5_series(port, psk, int(i), 2048)
+            rm, rc = port.rts_run(m, ys)
+            e = max_rel_err(d[f"m{i}"], d[f"c{i}"], rm, rc)
+            assert e < 1e-9, (r, int(i), e)
+            seen.append(int(i))
+    assert sorted(seen) == list(range(5))  # every series exactly once
+
+
+def _ptfs_worker(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200 import distributed as dp
+    from paper_2511_10363_b200.synthetic import cv_model
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    groups = dp.ptfs_groups(world)
+    dev = torch.device("cuda", 0)
+    m, ys = cv_model(T, seed=23)
+    fwd, i, h = dp.ptfs_halves(rank, world)
+    lo, hi = dp.shard_range(T, i, h)
+    ms, yss = dp.shard_model(m, ys, lo, hi, device=dev)
+    be = psk.CudaBackend(0)
+    out = dp.ptfs_run_sharded(ms, yss, psk.ScanSpec(psk.ScanAlg.DecoupledLookback, 16), be,
+                              rank, world, lo, hi, groups)
+    torch.cuda.synchronize()
+    if out is not None:
+        np.savez(Path(out_dir) / f"p{i}.npz", mean=out.mean.cpu().numpy(),
+                 cov=out.cov.cpu().numpy(), lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ptfs_halves_processes(gpu, tmp_path, port, world):
+    """configs[2] shape: the two-filter smoother with the forward filter on
+    one half of the ranks and the backward filter on the other (each half
+    time-sharded), real processes and collectives, T = 2^20, vs rts_run."""
+    import torch.multiprocessing as mp
+
+    from paper_2511_10363_b200.synthetic import cv_model
+    mp.spawn(_ptfs_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    m, ys = cv_model(T, seed=23)
+    rm, rc = port.rts_run(m, ys)
+    covered = 0
+    for i in range(world // 2):
+        d = np.load(tmp_path / f"p{i}.npz")
+        lo, hi = int(d["lo"]), int(d["hi"])
+        assert lo == covered
+        covered = hi
+        e = max_rel_err(d["mean"], d["cov"], rm[lo:hi], rc[lo:hi])
+        assert e < 1e-9, (i, e)
+    assert covered == T

@@ -127,7 +127,7 @@ def test_wide_path_all_methods(psk, gpu, port, nx, ny, chunk):
     assert max_rel_err(got.mean, got.cov, *rts) < TOL64, "ptfs"
     be.set_profile(True)
     psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg(6)), be)
-    assert any(n.startswith("wide_") for n, _ in be.last_profile())
+    assert any(n.startswith(("wide_", "tile_")) for n, _ in be.last_profile())
 
 
 def test_wide_path_large_t(psk, gpu, port):

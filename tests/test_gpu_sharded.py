@@ -72,3 +72,116 @@ def test_shard_requires_device_inputs(gpu, port):
     be = psk.CudaBackend(gpu)
     with pytest.raises(ValueError):
         CudaShardEngine(be, m, ys, 3, 10)
+
+
+def _virtual_sharded_ptfs(psk, m, ys, h, chunk, alg, gpu):
+    """The sharded PTFS (distributed.ptfs_sharded) with 2h virtual ranks on one
+    GPU: h forward shard engines (PSK_SHARD_FILTERED) and h backward ones over
+    the same step ranges; the exchanges done in-process."""
+    import torch
+
+    from paper_2511_10363_b200 import _lib
+    from paper_2511_10363_b200.distributed import (CudaShardEngine, shard_flags, shard_model,
+                                                   shard_range)
+    T = m.t
+    dev = torch.device("cuda", gpu)
+    spec = psk.ScanSpec(psk.ScanAlg(alg), 4)
+    fwd, bwd, spans = [], [], []
+    for i in range(h):
+        lo, hi = shard_range(T, i, h)
+        ms, yss = shard_model(m, ys, lo, hi, device=dev)
+        f = shard_flags(i, h)
+        fwd.append(CudaShardEngine(psk.CudaBackend(gpu, chunk=chunk), ms, yss,
+                                   f | _lib.PSK_SHARD_FILTERED, hi - lo))
+        bwd.append(CudaShardEngine(psk.CudaBackend(gpu, chunk=chunk), ms, yss, f, hi - lo))
+        spans.append((lo, hi))
+    a = [e.filter_reduce(spec) for e in fwd]
+    s = [e.backward_reduce(spec) for e in bwd]
+    out = []
+    for i in range(h):
+        t = spans[i][1] - spans[i][0]
+        fm, fc = fwd[i].stats(t)
+        fwd[i].filter_finish(fwd[i].fold("filter", a[:i]) if i > 0 else None, fm, fc)
+        carry = bwd[i].fold("backward", s[i + 1:]) if i < h - 1 else None
+        mean, cov = bwd[i].stats(t)
+        bwd[i].backward_finish(carry, fm, fc, mean, cov)
+        out.append((mean.cpu().numpy(), cov.cpu().numpy()))
+    return np.concatenate([o[0] for o in out]), np.concatenate([o[1] for o in out])
+
+
+@pytest.mark.parametrize("h", [1, 2, 4])
+@pytest.mark.parametrize("alg,chunk", [(6, 8), (3, 4), (2, 1)])
+def test_virtual_sharded_ptfs_halves(gpu, port, h, alg, chunk):
+    """PTFS on disjoint halves of 2h virtual ranks (each half time-sharded in
+    h shards) matches the sequential RTS oracle, like the one-context PTFS
+    (test_kalman_par.cpp:209-227: ptfs == rts at 1e-9)."""
+    import paper_2511_10363_b200 as psk
+    m, ys = gen(port, 40 + h, 4, 2, 777)
+    rts = port.rts_run(m, ys)
+    mean, cov = _virtual_sharded_ptfs(psk, m, ys, h, chunk, alg, gpu)
+    assert max_rel_err(mean, cov, *rts) < 1e-9
+    one = psk.ptfs_run(m, ys, psk.ScanSpec(psk.ScanAlg(alg), 4),
+                       psk.CudaBackend(gpu, chunk=chunk))
+    assert max_rel_err(mean, cov, one.mean, one.cov) < 1e-12
+
+
+def test_virtual_sharded_ptfs_tracking_large(gpu, port):
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200.synthetic import cv_model
+    m, ys = cv_model(1 << 18, seed=6)
+    rts = port.rts_run(m, ys)
+    mean, cov = _virtual_sharded_ptfs(psk, m, ys, 4, 32, 6, gpu)
+    assert max_rel_err(mean, cov, *rts) < 1e-9
+
+
+@pytest.mark.parametrize("devs", [[0, 0], [0, 0, 0], [0, 0, 0, 0], [0] * 8])
+def test_multi_device_context(gpu, port, devs):
+    """psk_create_multi: one process driving several members (streams of the
+    one GPU here; separate GPUs over NVLink on a multi-GPU box): PKF / PRTS
+    time-sharded over the members, PTFS on the two halves, host and device
+    inputs, against the sequential oracle (1e-9)."""
+    import torch
+
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200.synthetic import cv_model
+    m, ys = gen(port, 50 + len(devs), 4, 2, 3001)
+    kf = port.kf_run(m, ys)
+    rts = port.rts_run(m, ys)
+    be = psk.CudaBackend(devs)
+    for alg in (6, 3):
+        spec = psk.ScanSpec(psk.ScanAlg(alg), 16)
+        got = psk.prts_run(m, ys, spec, be)
+        assert max_rel_err(got.mean, got.cov, *rts) < 1e-9, ("prts", alg)
+        got = psk.pkf_run(m, ys, spec, be)
+        assert max_rel_err(got.mean, got.cov, *kf) < 1e-9, ("pkf", alg)
+        got = psk.ptfs_run(m, ys, spec, be, be, len(devs))
+        assert max_rel_err(got.mean, got.cov, *rts) < 1e-9, ("ptfs", alg)
+    assert be.last_launch_count() > 0
+    # device-space inputs and outputs
+    dev = torch.device("cuda", gpu)
+    mc, yc = cv_model(1 << 16, seed=9)
+    want = port.rts_run(mc, yc)
+    md = psk.Lgssm(**{k: torch.as_tensor(getattr(mc, k), device=dev)
+                      for k in ("f", "u", "q", "h", "d", "r", "prior_mean", "prior_cov")},
+                   t=mc.t)
+    got = psk.prts_run(md, torch.as_tensor(yc, device=dev),
+                       psk.ScanSpec(psk.ScanAlg.DecoupledLookback), be)
+    assert max_rel_err(got.mean.cpu(), got.cov.cpu(), *want) < 1e-9
+
+
+def test_multi_device_batch_and_fallbacks(gpu, port):
+    """Batches on a multi-device context are split between the members; dims
+    without shard phases (nx > 4) and tiny series run on the first member."""
+    import paper_2511_10363_b200 as psk
+    be = psk.CudaBackend([0, 0])
+    series = [gen(port, 60 + i, 4, 2, 500 + 37 * i) for i in range(5)]
+    outs = psk.prts_run_batch([s[0] for s in series], [s[1] for s in series],
+                              psk.ScanSpec(psk.ScanAlg.DecoupledLookback), be)
+    for (m, ys), o in zip(series, outs):
+        assert max_rel_err(o.mean, o.cov, *port.rts_run(m, ys)) < 1e-9
+    m, ys = gen(port, 70, 8, 4, 300)
+    got = psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg.InplaceLaFi), be)
+    assert max_rel_err(got.mean, got.cov, *port.rts_run(m, ys)) < 1e-9
+    m, ys = gen(port, 71, 4, 2, 1)
+    got = psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg.InplaceLaFi), be)
+    assert max_rel_err(got.mean, got.cov, *port.rts_run(m, ys)) < 1e-9

@@ -17,6 +17,11 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 
 
+def _np(x):
+    """numpy view of a (CPU) torch tensor the engine fills in place"""
+    return x.numpy() if hasattr(x, "numpy") else x
+
+
 class OracleShardEngine:
     """Reference-algorithm shard phases on the CPU (tests only)."""
 
@@ -44,6 +49,11 @@ class OracleShardEngine:
             for e in els[1:]:
                 acc = self.o.filter_combine(nx, acc, e)
             b, c = acc[nx * nx:nx * nx + nx], acc[nx * nx + nx:2 * nx * nx + nx]
+        elif kind == "backward":
+            acc = els[0]
+            for e in els[1:]:
+                acc = self.o.filter_combine(nx, acc, e)
+            b, c = acc[2 * nx * nx + nx:2 * nx * nx + 2 * nx], acc[2 * nx * nx + 2 * nx:]
         else:
             acc = els[-1]
             for e in els[-2::-1]:
@@ -52,7 +62,8 @@ class OracleShardEngine:
         return self._t(np.concatenate([b, c]))
 
     def stats(self, t):
-        return np.zeros((t, self.nx)), np.zeros((t, self.nx, self.nx))
+        return (self.torch.zeros((t, self.nx), dtype=self.torch.float64),
+                self.torch.zeros((t, self.nx, self.nx), dtype=self.torch.float64))
 
     def _slice(self, prior=None):
         from paper_2511_10363_b200.api import Lgssm
@@ -70,9 +81,10 @@ class OracleShardEngine:
             prior = (c[:nx].copy(), c[nx:].reshape(nx, nx).copy())
         sm, sys_ = self._slice(prior)
         fm, fc = self.o.kf_run(sm, sys_)
-        mean[:], cov[:] = fm, fc
+        _np(mean)[:], _np(cov)[:] = fm, fc
 
     def smoother_reduce(self, spec, mean, cov):
+        mean, cov = _np(mean), _np(cov)
         acc = None
         for i in range(self.hi - 1, self.lo - 1, -1):
             e = self.o.make_smoother_element(self.m, self.ys, mean[i - self.lo],
@@ -80,8 +92,46 @@ class OracleShardEngine:
             acc = e if acc is None else self.o.smoother_combine(self.nx, e, acc)
         return self._t(acc)
 
+    # ---- the backward half of a sharded PTFS (kalman_par.hpp:63-89, 183-201)
+    def _shifted(self, j):
+        """slot j (0-based) holds a(step j+1): make_filter_element with the
+        1-based step j + 2; identity past the series' last transition."""
+        nx = self.nx
+        if j + 1 < int(self.m.t):
+            return self.o.make_filter_element(self.m, self.ys, j + 2)
+        e = np.zeros(3 * nx * nx + 2 * nx)
+        e[:nx * nx] = np.eye(nx).ravel()
+        return e
+
+    def backward_reduce(self, spec):
+        acc = None
+        for j in range(self.lo, self.hi):
+            e = self._shifted(j)
+            acc = e if acc is None else self.o.filter_combine(self.nx, acc, e)
+        return self._t(acc)
+
+    def backward_finish(self, carry, fmean, fcov, mean, cov):
+        nx = self.nx
+        state = None
+        if carry is not None:  # (eta, J) only: an identity element carrying them
+            c = np.asarray(carry)
+            state = np.zeros(3 * nx * nx + 2 * nx)
+            state[:nx * nx] = np.eye(nx).ravel()
+            state[2 * nx * nx + nx:2 * nx * nx + 2 * nx] = c[:nx]
+            state[2 * nx * nx + 2 * nx:] = c[nx:]
+        fm, fc = _np(fmean), _np(fcov)
+        mean, cov = _np(mean), _np(cov)
+        for j in range(self.hi - 1, self.lo - 1, -1):
+            e = self._shifted(j)
+            state = e if state is None else self.o.filter_combine(nx, e, state)
+            eta = state[2 * nx * nx + nx:2 * nx * nx + 2 * nx].copy()
+            jm = state[2 * nx * nx + 2 * nx:].reshape(nx, nx).copy()
+            x, p = self.o.tf_combine(fm[j - self.lo].copy(), fc[j - self.lo].copy(), eta, jm)
+            mean[j - self.lo], cov[j - self.lo] = x, p
+
     def smoother_finish(self, carry, mean, cov):
         nx = self.nx
+        mean, cov = _np(mean), _np(cov)
         state = None
         if carry is not None:
             c = np.asarray(carry)
@@ -174,3 +224,54 @@ def test_shard_model_slices_with_boundary_transition():
     assert ml.t == 4 and torch.equal(ml.f, torch.as_tensor(f[6:10]))
     m32, _ = shard_model(m, ys, 0, 5, dtype=torch.float32)
     assert m32.f.dtype == torch.float32
+
+
+
+def _ptfs_worker(rank, world, port, t, out_dir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+
+    from conftest import gen
+    from oracle.oracle import Oracle
+    from paper_2511_10363_b200.api import ScanSpec
+    from paper_2511_10363_b200.distributed import (ptfs_groups, ptfs_halves, ptfs_sharded,
+                                                   shard_range)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    groups = ptfs_groups(world)
+    orc = Oracle("port")
+    m, ys = gen(orc, 14, 4, 2, t)
+    fwd, i, h = ptfs_halves(rank, world)
+    lo, hi = shard_range(t, i, h)
+    eng = OracleShardEngine(orc, m, ys, lo, hi)
+    out = ptfs_sharded(eng, ScanSpec(), rank, world, hi - lo, groups)
+    if out is not None:
+        np.savez(Path(out_dir) / f"p{i}.npz", mean=np.asarray(out[0]), cov=np.asarray(out[1]),
+                 lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,t", [(2, 37), (4, 61), (6, 50)])
+def test_sharded_ptfs_halves_matches_rts(tmp_path, port, world, t):
+    """PTFS with the forward filter time-sharded over ranks [0, G/2) and the
+    backward filter over [G/2, G) (distributed.ptfs_sharded) reproduces the
+    sequential RTS smoother (the reference checks ptfs against rts_run at
+    1e-9, test_kalman_par.cpp:209-227)."""
+    import torch.multiprocessing as mp
+
+    from conftest import gen, max_rel_err
+    mp.spawn(_ptfs_worker, args=(world, _free_port(), t, str(tmp_path)), nprocs=world,
+             join=True)
+    m, ys = gen(port, 14, 4, 2, t)
+    rm, rc = port.rts_run(m, ys)
+    covered = 0
+    for i in range(world // 2):
+        d = np.load(tmp_path / f"p{i}.npz")
+        lo, hi = int(d["lo"]), int(d["hi"])
+        assert lo == covered
+        covered = hi
+        assert max_rel_err(d["mean"], d["cov"], rm[lo:hi], rc[lo:hi]) < 1e-9, i
+    assert covered == t
