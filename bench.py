@@ -417,9 +417,11 @@ def run_psk(args) -> None:
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             out = step()
             launches += be.last_launch_count()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue cost per step
         ev1.record(stream)
         torch.cuda.synchronize()
     be.sync()  # raises on any device error of the timed steps
@@ -495,6 +497,7 @@ def run_psk(args) -> None:
             "dtype": args.dtype, "data": "synthetic", "config": config(args),
             "roofline": roof, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels,
+            "host_enqueue_ms_per_step": round(host_ms, 3),
         }
         print(json.dumps(line), flush=True)
     if pg is not None:

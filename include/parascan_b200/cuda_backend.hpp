@@ -149,10 +149,24 @@ inline bool block_dims_ok(const Vec<S>& a, std::size_t r, std::size_t) {
   return std::size_t(a.len()) == r;
 }
 
-// Lgssm<S> (per-step std::vector<Mat>) -> per-field dense arrays in the
-// backend's pinned input buffer (one field after another, 16-byte aligned)
+// scalars of the packed per-field arrays of a model (16-byte aligned fields)
 template <typename S>
-psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
+std::size_t packed_size(const Lgssm<S>& m) {
+  const std::size_t nx = std::size_t(m.nx), ny = std::size_t(m.ny), t = m.t;
+  const std::size_t blk[9] = {nx * nx, nx, nx * nx, ny * nx, ny, ny * ny, ny, nx, nx * nx};
+  const std::size_t align = 16 / sizeof(S);
+  std::size_t total = 0;
+  for (int i = 0; i < 9; ++i) {
+    const std::size_t n = i < 7 ? blk[i] * t : blk[i];
+    total += (n + align - 1) / align * align;
+  }
+  return total;
+}
+
+// Lgssm<S> (per-step std::vector<Mat>) -> per-field dense arrays at `base`
+// (packed_size(m) scalars; one field after another, 16-byte aligned)
+template <typename S>
+psk_model pack_into(const Lgssm<S>& m, const Measurements<S>& ys, S* base) {
   const std::size_t nx = std::size_t(m.nx), ny = std::size_t(m.ny), t = m.t;
   if (m.f.size() != t || m.u.size() != t || m.q.size() != t || m.h.size() != t ||
       m.d.size() != t || m.r.size() != t || ys.size() != t)
@@ -167,7 +181,6 @@ psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
     const std::size_t n = i < 7 ? blk[i] * t : blk[i];
     total += (n + align - 1) / align * align;
   }
-  S* base = static_cast<S*>(buf.reserve(sizeof(S) * (total ? total : 1)));
   parallel_for(t, 1 << 14, [&](std::size_t lo, std::size_t hi) {
     auto put = [&](int i, const auto& src, std::size_t r, std::size_t c) {
       S* dst = base + off[i];
@@ -203,21 +216,44 @@ psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
   return md;
 }
 
-// raw outputs mean[T][nx], cov[T][nx][nx] -> vector<GaussianStats<S>>; every
-// step's Vec / Mat is allocated by the worker that fills it
+// the same into the backend's pinned input buffer
 template <typename S>
-std::vector<GaussianStats<S>> unpack(const S* mean, const S* cov, std::size_t t, int nx) {
+psk_model pack(const Lgssm<S>& m, const Measurements<S>& ys, Pinned& buf) {
+  return pack_into(m, ys, static_cast<S*>(buf.reserve(sizeof(S) * (packed_size(m) + 1))));
+}
+
+// The output vector<GaussianStats<S>> of t steps with every step's Vec / Mat
+// allocated (by the worker that will fill it: first-touch locality).  The
+// per-step heap objects are the reference's return type (lgssm.hpp:18-21);
+// allocating 2 t of them is the single largest host cost of a drop-in call,
+// so call() builds them on a separate thread while it packs the inputs and
+// the device runs.
+template <typename S>
+std::vector<GaussianStats<S>> alloc_stats(std::size_t t, int nx) {
   std::vector<GaussianStats<S>> out(t);
-  const std::size_t n = std::size_t(nx);
   parallel_for(t, 1 << 13, [&](std::size_t lo, std::size_t hi) {
     for (std::size_t k = lo; k < hi; ++k) {
-      GaussianStats<S>& g = out[k];
-      g.mean = Vec<S>(nx);
-      g.cov = Mat<S>(nx, nx);
-      std::memcpy(g.mean.view().d, mean + k * n, sizeof(S) * n);
-      std::memcpy(g.cov.data(), cov + k * n * n, sizeof(S) * n * n);
+      out[k].mean = Vec<S>(nx);
+      out[k].cov = Mat<S>(nx, nx);
     }
   });
+  return out;
+}
+// raw outputs mean[T][nx], cov[T][nx][nx] -> the allocated per-step objects
+template <typename S>
+void fill_stats(std::vector<GaussianStats<S>>& out, const S* mean, const S* cov, int nx) {
+  const std::size_t n = std::size_t(nx);
+  parallel_for(out.size(), 1 << 13, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t k = lo; k < hi; ++k) {
+      std::memcpy(out[k].mean.view().d, mean + k * n, sizeof(S) * n);
+      std::memcpy(out[k].cov.data(), cov + k * n * n, sizeof(S) * n * n);
+    }
+  });
+}
+template <typename S>
+std::vector<GaussianStats<S>> unpack(const S* mean, const S* cov, std::size_t t, int nx) {
+  std::vector<GaussianStats<S>> out = alloc_stats<S>(t, nx);
+  fill_stats(out, mean, cov, nx);
   return out;
 }
 
@@ -226,10 +262,21 @@ inline void check_dims(int nx, int ny) {
 }
 
 // vector<GaussianStats> outputs: raw results land in the pinned output buffer
+// The output objects are allocated on a helper thread while this thread
+// packs the inputs and the device computes (pack -> H2D -> kernels -> D2H);
+// only the copy into them remains after the call.
 template <typename S, class F>
 std::vector<GaussianStats<S>> call(const Lgssm<S>& m, const Measurements<S>& ys,
                                    CudaBackend& be, F&& f) {
   check_dims(m.nx, m.ny);
+  std::vector<GaussianStats<S>> out;
+  std::thread alloc([&] { out = alloc_stats<S>(m.t, m.nx); });
+  struct Join {
+    std::thread& th;
+    ~Join() {
+      if (th.joinable()) th.join();
+    }
+  } join{alloc};
   const psk_model md = pack(m, ys, be.staging_in());
   const std::size_t nm = m.t * std::size_t(m.nx), nc = nm * std::size_t(m.nx);
   const std::size_t mb = (sizeof(S) * nm + 15) / 16 * 16;
@@ -237,7 +284,9 @@ std::vector<GaussianStats<S>> call(const Lgssm<S>& m, const Measurements<S>& ys,
   S* mean = reinterpret_cast<S*>(o);
   S* cov = reinterpret_cast<S*>(o + mb);
   check(f(md, mean, cov));
-  return unpack(mean, cov, m.t, m.nx);
+  alloc.join();
+  fill_stats(out, mean, cov, m.nx);
+  return out;
 }
 
 // caller-owned SoA outputs (mean[T][nx], cov[T][nx][nx], host memory)

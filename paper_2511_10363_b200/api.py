@@ -405,11 +405,11 @@ def _ordered_call(bes: list[CudaBackend], mks: list[_Marshal], outs: list[Any], 
 
     The contexts run on their own streams.  For device-space (CUDA tensor)
     models their streams first wait for torch's current stream (inputs and the
-    contiguous copies _Marshal made are produced there), torch's stream then
-    waits for theirs (the outputs), and every tensor the call reads or writes
-    is recorded on the context streams so the caching allocator cannot hand
-    its memory out while a queued (async mode) kernel still uses it.  Host
-    marshals of async calls are kept alive until sync()."""
+    contiguous copies _Marshal made are produced there), and torch's stream
+    then waits for theirs, so the outputs are ready for torch and memory the
+    caching allocator hands out again on torch's stream is not overwritten
+    while a queued (async mode) kernel still uses it.  Host marshals of async
+    calls are kept alive until sync()."""
     dev = next((mk.device for mk in mks if mk.device is not None), None)
     if dev is None:
         call()
@@ -433,15 +433,13 @@ def _ordered_call(bes: list[CudaBackend], mks: list[_Marshal], outs: list[Any], 
             ext.wait_stream(cur)
             exts.append(ext)
     call()
+    # torch's stream waits for the context's: later torch work on the outputs,
+    # and any reuse by the caching allocator of the inputs' / temporaries'
+    # memory (allocations on this stream), is ordered after the psk kernels.
+    # (No record_stream on the context stream: the allocator would record
+    # events on it when the tensors die, possibly after psk_destroy.)
     for ext in exts:
         cur.wait_stream(ext)
-        for mk in mks:
-            for t in mk.keep:
-                if _is_torch(t) and t.device.type == "cuda":
-                    t.record_stream(ext)
-        for t in outs:
-            if t.device.type == "cuda":
-                t.record_stream(ext)
 
 
 def _run(entry: str, m: Lgssm, ys: Any, spec: ScanSpec, be: CudaBackend,

@@ -95,6 +95,14 @@ inline size_t dlb_state_bytes(long long n) {
   return dlb_head_bytes(nt) + sizeof(S) * (size_t)nt * (2 * kDlbStride + fs * kDlbThreads);
 }
 
+// The warp-shuffle tile scan needs two elements in registers per thread:
+// used where they fit (FP32 elements, the 36-scalar FP64 smoothing element);
+// the 56-double filtering element keeps the shared-memory sweeps.
+template <class Ops>
+constexpr bool dlb_shuffle() {
+  return Ops::kSize * sizeof(typename Ops::S) <= 320;
+}
+
 template <class Ops>
 __global__ void __launch_bounds__(kDlbThreads)
     k_dlb(Ops ops, typename Ops::S* buf, long long n, long long cap, int rev, int perm,
@@ -147,24 +155,53 @@ __global__ void __launch_bounds__(kDlbThreads)
   }
   __syncthreads();
   dlb_stamp(trace, tile, 1);
-  // 3. tile scan of the thread aggregates: up-sweep, then Ladner-Fischer down
+  // 3. tile scan of the thread aggregates
+  if constexpr (dlb_shuffle<Ops>()) {
+    // warp-shuffle scans: Hillis-Steele (Kogge-Stone) over the 32 lanes of
+    // each warp with the elements in registers (scan.hpp:214-259's index map
+    // at warp scope, 5 levels, no barriers), then every warp applies the
+    // ordered fold of the earlier warps' totals from shared memory
+    const int lane = t & 31, w = t >> 5;
+    auto x = ops.get(sb, t);
 #pragma unroll 1
-  for (int d = 0; d < kDlbLevels; ++d) {
-    const int d1 = 1 << d, d2 = d1 << 1;
-    if (t < kDlbThreads / d2) {
-      const int j = t * d2 + d1 - 1, k = t * d2 + d2 - 1;
-      lcomb(sb, k, sb, j, sb, k);
+    for (int d = 1; d < 32; d <<= 1) {
+      const auto y = Ops::shfl(x, [&](S v) { return __shfl_up_sync(0xffffffffu, v, d); });
+      if (lane >= d) x = rev ? ops.comb(x, y) : ops.comb(y, x);
+    }
+    ops.put(sb, t, x);
+    __syncthreads();
+    if (w > 0) {
+      auto p = ops.get(sb, 31);
+#pragma unroll 1
+      for (int v = 1; v < w; ++v) {
+        const auto q = ops.get(sb, 32 * v + 31);
+        p = rev ? ops.comb(q, p) : ops.comb(p, q);
+      }
+      x = rev ? ops.comb(x, p) : ops.comb(p, x);
     }
     __syncthreads();
-  }
-#pragma unroll 1
-  for (int d = kDlbLevels - 1; d >= 0; --d) {
-    const int d1 = 1 << d, d2 = d1 << 1, blocks = kDlbThreads / d2;
-    if (blocks > 1 && t < blocks - 1) {
-      const int i = (t + 1) * d2 - 1, j = i + d1;
-      lcomb(sb, j, sb, i, sb, j);
-    }
+    if (w > 0) ops.put(sb, t, x);
     __syncthreads();
+  } else {
+    // up-sweep, then Ladner-Fischer down-sweep in shared memory
+#pragma unroll 1
+    for (int d = 0; d < kDlbLevels; ++d) {
+      const int d1 = 1 << d, d2 = d1 << 1;
+      if (t < kDlbThreads / d2) {
+        const int j = t * d2 + d1 - 1, k = t * d2 + d2 - 1;
+        lcomb(sb, k, sb, j, sb, k);
+      }
+      __syncthreads();
+    }
+#pragma unroll 1
+    for (int d = kDlbLevels - 1; d >= 0; --d) {
+      const int d1 = 1 << d, d2 = d1 << 1, blocks = kDlbThreads / d2;
+      if (blocks > 1 && t < blocks - 1) {
+        const int i = (t + 1) * d2 - 1, j = i + d1;
+        lcomb(sb, j, sb, i, sb, j);
+      }
+      __syncthreads();
+    }
   }
   dlb_stamp(trace, tile, 2);
   // 4. publish the tile aggregate (tile 0: its inclusive prefix); park the

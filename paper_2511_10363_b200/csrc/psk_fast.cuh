@@ -242,11 +242,42 @@ __device__ __forceinline__ SElem<S, NX> smoother_combine(const SElem<S, NX>& l,
 }
 
 // ---- level-scan operator policies ----------------------------------------
+// component-wise warp shuffle of a register matrix: y = f(x) per entry
+template <typename S, int R, int C, class Shfl>
+__device__ __forceinline__ void shfl_mat(Mat<S, R, C>& y, const Mat<S, R, C>& x, Shfl&& f) {
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < C; ++j) y.a[i][j] = f(x.a[i][j]);
+}
+
 template <typename S_, int NX>
 struct FastFilterOps {
   using S = S_;
+  using Elem = FElem<S, NX>;
   static constexpr int kSize = FLayout<NX>::size;
   unsigned* err;
+  // register-level interface (the DLB's warp-shuffle scans, psk_dlb.cuh)
+  __device__ Elem get(const ElemBuf<S>& b, long long i) const { return fe_load<S, NX>(b.p, b.cap, i); }
+  __device__ void put(const ElemBuf<S>& b, long long i, const Elem& x) const {
+    fe_store(b.p, b.cap, i, x);
+  }
+  __device__ Elem comb(const Elem& l, const Elem& r) const {
+    unsigned e = 0;
+    const Elem o = filter_combine(l, r, e);
+    if (e) atomicOr(err, e);
+    return o;
+  }
+  template <class Shfl>
+  __device__ static Elem shfl(const Elem& x, Shfl&& f) {
+    Elem y;
+    shfl_mat(y.A, x.A, f);
+    shfl_mat(y.b, x.b, f);
+    shfl_mat(y.C, x.C, f);
+    shfl_mat(y.eta, x.eta, f);
+    shfl_mat(y.J, x.J, f);
+    return y;
+  }
   __device__ void combine(const ElemBuf<S>& d, long long di,
                           const ElemBuf<S>& l, long long li,
                           const ElemBuf<S>& r, long long ri) const {
@@ -269,8 +300,22 @@ struct FastFilterOps {
 template <typename S_, int NX>
 struct FastSmootherOps {
   using S = S_;
+  using Elem = SElem<S, NX>;
   static constexpr int kSize = SLayout<NX>::size;
   unsigned* err;
+  __device__ Elem get(const ElemBuf<S>& b, long long i) const { return se_load<S, NX>(b.p, b.cap, i); }
+  __device__ void put(const ElemBuf<S>& b, long long i, const Elem& x) const {
+    se_store(b.p, b.cap, i, x);
+  }
+  __device__ Elem comb(const Elem& l, const Elem& r) const { return smoother_combine(l, r); }
+  template <class Shfl>
+  __device__ static Elem shfl(const Elem& x, Shfl&& f) {
+    Elem y;
+    shfl_mat(y.E, x.E, f);
+    shfl_mat(y.g, x.g, f);
+    shfl_mat(y.L, x.L, f);
+    return y;
+  }
   __device__ void combine(const ElemBuf<S>& d, long long di,
                           const ElemBuf<S>& l, long long li,
                           const ElemBuf<S>& r, long long ri) const {
