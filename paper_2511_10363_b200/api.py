@@ -498,9 +498,9 @@ def _run_batch(entry: str, models: list[Lgssm], ys_list: list[Any], spec: ScanSp
         mean, cov = _outputs(mk, None if outs is None else outs[i])
         mks.append(mk)
         res.append(GaussianStats(mean, cov))
-    devs = {mk.device for mk in mks}
+    devs = {mk.device for mk in mks if mk.device is not None}
     if len(devs) > 1:
-        raise ValueError("a batch must be all host-space or all on one CUDA device")
+        raise ValueError("the device-space series of a batch must share one CUDA device")
     n = len(mks)
     arr = (_lib.psk_model * max(n, 1))(*[mk.model for mk in mks])
     pm = (C.c_void_p * max(n, 1))(*[mks[i]._ptr(res[i].mean) for i in range(n)])
@@ -509,8 +509,7 @@ def _run_batch(entry: str, models: list[Lgssm], ys_list: list[Any], spec: ScanSp
 
     def call():
         _check(fn(be.handle, arr, n, int(spec.alg), int(spec.sengupta_n), pm, pc))
-    tens = [t for r in res for t in (r.mean, r.cov)] if mks and mks[0].torch else []
-    _ordered_call([be], mks, tens, call)
+    _ordered_call([be], mks, [], call)
     return res
 
 
