@@ -33,7 +33,17 @@
 namespace psk {
 namespace tile {
 
-__device__ __forceinline__ int lane() { return threadIdx.x & 31; }
+// Lanes per chunk: a HALF warp works on one chunk, so every warp carries two
+// chunks and a 16 x 16 product gives each lane a 4 x 4 tile (0.5 operand
+// loads per FMA instead of 0.75 for 2 x 4 tiles on a full warp -- the kernels
+// are bound by shared-memory -> register bandwidth).
+constexpr int kGW = 16;
+// lane within the chunk's group, the group's mask, group-wide sync
+__device__ __forceinline__ int lane() { return threadIdx.x & (kGW - 1); }
+__device__ __forceinline__ unsigned gmask() {
+  return kGW == 32 ? 0xffffffffu : (((1u << kGW) - 1u) << (threadIdx.x & 31 & ~(kGW - 1)));
+}
+__device__ __forceinline__ void gsync() { __syncwarp(gmask()); }
 
 template <typename S>
 constexpr int vec16() {
@@ -89,13 +99,13 @@ __device__ __forceinline__ void st(S* p, const S (&v)[n]) {
   }
 }
 
-// Output tiling of an M x N result over the warp: lane -> tile (tr, tc) of
-// TM x TN; lanes >= TR * TC hold no tile.
+// Output tiling of an M x N result over the chunk's lane group: lane -> tile
+// (tr, tc) of TM x TN; lanes >= TR * TC hold no tile.
 template <int M, int N, int TM, int TN>
 struct Tiling {
   static constexpr int TR = M / TM, TC = N / TN, tiles = TR * TC;
-  static_assert(M % TM == 0 && N % TN == 0 && tiles <= 32, "tiling");
-  __device__ __forceinline__ static bool active() { return tiles == 32 || lane() < tiles; }
+  static_assert(M % TM == 0 && N % TN == 0 && tiles <= kGW, "tiling");
+  __device__ __forceinline__ static bool active() { return tiles == kGW || lane() < tiles; }
   __device__ __forceinline__ static int r0() { return (lane() / TC) * TM; }
   __device__ __forceinline__ static int c0() { return (lane() % TC) * TN; }
 };
@@ -185,18 +195,18 @@ __device__ __forceinline__ void neg(S (&acc)[TM][TN]) {
 
 // Gauss-Jordan elimination without pivoting on the R x W block X (row stride
 // LDX): [A | B] -> [I | A^-1 B] for A symmetric positive definite.  Lane l
-// holds columns l, l + 32, ... in registers; the pivot column is published by
+// of the group holds columns l, l + kGW, ... in registers; the pivot column is published by
 // its owner lane through pv (2 R scalars, double-buffered) and read back by
 // every lane as broadcast vector loads.
 template <int R, int W, int LDX, typename S>
 __device__ __forceinline__ void gj_spd(S* X, S* pv, unsigned& err) {
-  constexpr int NC = (W + 31) / 32;
-  static_assert(R <= 32, "pivot column owner");
+  constexpr int NC = (W + kGW - 1) / kGW;
+  static_assert(R <= kGW, "pivot column owner");
   const int ln = lane();
   S x[NC][R];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const int col = ln + 32 * c;
+    const int col = ln + kGW * c;
 #pragma unroll
     for (int i = 0; i < R; ++i) x[c][i] = col < W ? X[i * LDX + col] : S(0);
   }
@@ -204,7 +214,7 @@ __device__ __forceinline__ void gj_spd(S* X, S* pv, unsigned& err) {
   for (int p = 0; p < R; ++p) {
     S* buf = pv + (p & 1) * R;
     if (ln == p) st<R, 1>(buf, x[0]);
-    __syncwarp();
+    gsync();
     S col[R];
     ld<R, 1>(col, buf);
     const S d = col[p];
@@ -221,13 +231,13 @@ __device__ __forceinline__ void gj_spd(S* X, S* pv, unsigned& err) {
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const int col = ln + 32 * c;
+    const int col = ln + kGW * c;
     if (col < W) {
 #pragma unroll
       for (int i = 0; i < R; ++i) X[i * LDX + col] = x[c][i];
     }
   }
-  __syncwarp();
+  gsync();
 }
 
 // y(r) = sum_k A(r, k) x(k) (+ z(r)), A(r, k) at a[r AR + k AK]; lanes r < n
@@ -269,7 +279,7 @@ __device__ __forceinline__ void load_model(S* mf, const ModelView<S>& m, long lo
   const S* F = m.F(k);
   const S* Q = m.Q(k);
 #pragma unroll
-  for (int i = ln; i < N * N; i += 32) {
+  for (int i = ln; i < N * N; i += kGW) {
     const int r = i / N, c = i % N;
     mf[MF::Fc + c * MF::LD + r] = F[i];
     mf[MF::Q + r * MF::LD + c] = Q[i];
@@ -278,13 +288,13 @@ __device__ __forceinline__ void load_model(S* mf, const ModelView<S>& m, long lo
   if (fqu_only) return;
   const S* H = m.H(k);
 #pragma unroll
-  for (int i = ln; i < M * N; i += 32) {
+  for (int i = ln; i < M * N; i += kGW) {
     const int r = i / N, c = i % N;
     mf[MF::Ht + c * MF::LDM + r] = H[i];
   }
   const S* Rg = m.R(k);
 #pragma unroll
-  for (int i = ln; i < M * M; i += 32) mf[MF::R + (i / M) * MF::LDR + (i % M)] = Rg[i];
+  for (int i = ln; i < M * M; i += kGW) mf[MF::R + (i / M) * MF::LDR + (i % M)] = Rg[i];
   if (ln < M) {
     mf[MF::d + ln] = m.D(k)[ln];
     mf[MF::y + ln] = m.Y(k)[ln];
@@ -304,7 +314,7 @@ __host__ __device__ __forceinline__ bool time_invariant(const ModelView<S>& m) {
 template <int N, int LDa, bool COLM, bool SYM, typename S>
 __device__ __forceinline__ void gstore_mat(S* g, const S* a) {
 #pragma unroll
-  for (int i = lane(); i < N * N; i += 32) {
+  for (int i = lane(); i < N * N; i += kGW) {
     int r = i / N, c = i % N;
     if (SYM && r > c) {
       const int t = r;
@@ -317,7 +327,7 @@ __device__ __forceinline__ void gstore_mat(S* g, const S* a) {
 template <int N, int LDa, bool COLM, typename S>
 __device__ __forceinline__ void sload_mat(S* a, const S* g) {
 #pragma unroll
-  for (int i = lane(); i < N * N; i += 32) {
+  for (int i = lane(); i < N * N; i += kGW) {
     const int r = i / N, c = i % N;
     if (COLM)
       a[c * LDa + r] = g[i];

@@ -20,28 +20,24 @@ namespace tile {
 using wide::FOffs;
 using wide::SOffs;
 
-// Lane tile of an M x N product: the largest of 4x4, 2x4, 1x4, 2x2, 1x2, 1x1
-// that still gives every lane a tile (or the finest tiling when there are
-// fewer than 32 outputs).
+// Lane tile of an M x N product over the kGW lanes of a chunk: the largest of
+// 4x8, 4x4, 2x4, 1x4, 2x2, 1x2, 1x1 that still gives every lane a tile (the
+// finest tiling when there are fewer than kGW outputs).
+constexpr bool tile_fits(int M, int N, int tm, int tn) {
+  return M % tm == 0 && N % tn == 0 && (M / tm) * (N / tn) >= kGW;
+}
 constexpr int pick_tm(int M, int N) {
-  return (M % 4 == 0 && N % 4 == 0 && (M / 4) * (N / 4) >= 32) ? 4
-         : (M % 2 == 0 && N % 4 == 0 && (M / 2) * (N / 4) >= 32) ? 2
-         : (N % 4 == 0 && M * (N / 4) >= 32) ? 1
-         : (M % 2 == 0 && N % 2 == 0 && (M / 2) * (N / 2) >= 32) ? 2
-         : 1;
+  return tile_fits(M, N, 4, 8) ? 4 : tile_fits(M, N, 4, 4) ? 4 : tile_fits(M, N, 2, 4) ? 2
+       : tile_fits(M, N, 1, 4) ? 1 : tile_fits(M, N, 2, 2) ? 2 : 1;
 }
 constexpr int pick_tn(int M, int N) {
-  return (M % 4 == 0 && N % 4 == 0 && (M / 4) * (N / 4) >= 32) ? 4
-         : (M % 2 == 0 && N % 4 == 0 && (M / 2) * (N / 4) >= 32) ? 4
-         : (N % 4 == 0 && M * (N / 4) >= 32) ? 4
-         : (M % 2 == 0 && N % 2 == 0 && (M / 2) * (N / 2) >= 32) ? 2
-         : (N % 2 == 0 && M * (N / 2) >= 32) ? 2
-         : 1;
+  return tile_fits(M, N, 4, 8) ? 8 : tile_fits(M, N, 4, 4) ? 4 : tile_fits(M, N, 2, 4) ? 4
+       : tile_fits(M, N, 1, 4) ? 4 : tile_fits(M, N, 2, 2) ? 2 : tile_fits(M, N, 1, 2) ? 2 : 1;
 }
 template <int M, int N>
 struct Pick {
   static constexpr int TM = pick_tm(M, N), TN = pick_tn(M, N);
-  static_assert((M / TM) * (N / TN) <= 32, "one tile per lane");
+  static_assert((M / TM) * (N / TN) <= kGW, "one tile per lane");
 };
 
 // ---- per-warp frames (scalars; every offset a whole number of 16 bytes) -------
@@ -77,12 +73,14 @@ struct SFrame {  // smoother finish
                        tmp = xs + up16<S>(N), g = tmp + up16<S>(N), size = g + up16<S>(N);
 };
 
-constexpr int kTileWarps = 4;  // warps (chunks) per CTA
+// chunks (lane groups) per CTA of each kernel: two CTAs per SM fit in shared
+// memory (reduce 12, finish 8, smoother finish 16 chunks per SM)
+constexpr int kGroupsReduce = 6, kGroupsFinish = 4, kGroupsSmooth = 8;
 
-template <typename S, int N, int M, int FR>
+template <typename S, int N, int M, int FR, int G>
 __host__ __device__ constexpr int cta_smem(bool invariant) {
   return (int)sizeof(S) *
-         (kTileWarps * (FR + (invariant ? 0 : ModelFrame<S, N, M>::size)) +
+         (G * (FR + (invariant ? 0 : ModelFrame<S, N, M>::size)) +
           (invariant ? ModelFrame<S, N, M>::size : 0));
 }
 
@@ -92,7 +90,7 @@ template <typename S, int N, int M, int FR>
 __device__ __forceinline__ void frames(const ModelView<S>& m, bool inv, S*& fr, S*& mf) {
   extern __shared__ __align__(16) unsigned char tsm[];
   S* base = reinterpret_cast<S*>(tsm);
-  const int w = threadIdx.x >> 5;
+  const int w = threadIdx.x / kGW;
   constexpr int MS = ModelFrame<S, N, M>::size;
   if (inv) {
     mf = base;
@@ -110,7 +108,7 @@ __device__ __forceinline__ void frames(const ModelView<S>& m, bool inv, S*& fr, 
 // warp-tiled products; from the identity (or the prior in state form for the
 // chunk holding step 1, kalman_elems.hpp:68-96).
 template <typename S, int N, int M>
-__global__ void __launch_bounds__(32 * kTileWarps)
+__global__ void __launch_bounds__(kGW * kGroupsReduce)
     k_t_reduce(ModelView<S> m, long long L, long long nchunks, S* agg, unsigned* err) {
   using RF = RFrame<S, N, M>;
   using MF = ModelFrame<S, N, M>;
@@ -118,7 +116,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
   const bool inv = time_invariant(m);
   S *fr, *mf;
   frames<S, N, M, RF::size>(m, inv, fr, mf);
-  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / kGW;
   if (c >= nchunks) return;  // warp-uniform (after the CTA barrier)
   const int ln = lane();
   unsigned e = 0;
@@ -136,7 +134,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
   S* tmp = fr + RF::tmp;
   S* vv = fr + RF::vv;
   S* pv = fr + RF::pv;
-  for (int i = ln; i < N * N; i += 32) {
+  for (int i = ln; i < N * N; i += kGW) {
     const int r = i / N, cc = i % N;
     A[r * LD + cc] = (!prior && r == cc) ? S(1) : S(0);
     C[r * LD + cc] = prior ? m.p0[i] : S(0);
@@ -146,7 +144,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
     b[ln] = prior ? m.m0[ln] : S(0);
     eta[ln] = S(0);
   }
-  __syncwarp();
+  gsync();
   const S* Fc = mf + MF::Fc;
   const S* Qm = mf + MF::Q;
   const S* Ht = mf + MF::Ht;
@@ -154,7 +152,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
   for (long long k = k0; k < k1; ++k) {
     if (!inv) {
       load_model<S, N, M>(mf, m, k);
-      __syncwarp();
+      gsync();
     }
     // predict the conditional: [A' | T] = F [A | C] (T = F C, column-major)
     {
@@ -174,7 +172,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
       }
       if (ln < N) tmp[ln] = mf[MF::u + ln] + matvec_row<N, N, 1, LD>(Fc, b, ln);
     }
-    __syncwarp();
+    gsync();
     {  // C = (F C) F^T + Q
       using P = Pick<N, N>;
       using TL = Tiling<N, N, P::TM, P::TN>;
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
       A = An;
       An = t;
     }
-    __syncwarp();
+    gsync();
     // [HC | HA] = H [C | A] -> HCA and the augmented block
     {
       using P = Pick<M, 2 * N>;
@@ -213,19 +211,19 @@ __global__ void __launch_bounds__(32 * kTileWarps)
         AUG[ln * LDA + M + 2 * N] = v;
       }
     }
-    __syncwarp();
+    gsync();
     {  // S = HC H^T + R
-      using TL = Tiling<M, M, (M >= 8 ? 2 : 1), 1>;
-      constexpr int TM = M >= 8 ? 2 : 1;
+      using P = Pick<M, M>;
+      using TL = Tiling<M, M, P::TM, P::TN>;
       if (TL::active()) {
         const int r0 = TL::r0(), c0 = TL::c0();
-        S acc[TM][1];
-        init<TM, 1, LDR, 1>(acc, Rm + r0 * LDR + c0);
-        mma<N, TM, 1, LDH, 1, LDM, 1>(acc, HCA + r0 * LDH, Ht + c0);
-        put_sym<TM, 1, LDA>(AUG, acc, r0, c0);
+        S acc[P::TM][P::TN];
+        init<P::TM, P::TN, LDR, 1>(acc, Rm + r0 * LDR + c0);
+        mma<N, P::TM, P::TN, LDH, 1, LDM, 1>(acc, HCA + r0 * LDH, Ht + c0);
+        put_sym<P::TM, P::TN, LDA>(AUG, acc, r0, c0);
       }
     }
-    __syncwarp();
+    gsync();
     gj_spd<M, M + 2 * N + 1, LDA>(AUG, pv, e);  // [I | K^T | S^-1 HA | S^-1 v]
     {  // J += HA^T S^-1 HA
       using P = Pick<N, N>;
@@ -255,19 +253,17 @@ __global__ void __launch_bounds__(32 * kTileWarps)
           put_sym<P::TM, P::TN, LD>(C, acc, r0, c0 - N);
       }
     }
-    if (ln < N) {  // b += K v
-      S s = b[ln];
+    if (ln < N) {  // b += K v ; eta += HA^T S^-1 v
+      S s = b[ln], h = eta[ln];
 #pragma unroll
-      for (int q = 0; q < M; ++q) s = sfma(AUG[q * LDA + M + ln], vv[q], s);
+      for (int q = 0; q < M; ++q) {
+        s = sfma(AUG[q * LDA + M + ln], vv[q], s);
+        h = sfma(HCA[q * LDH + RF::HAO + ln], AUG[q * LDA + M + 2 * N], h);
+      }
       b[ln] = s;
-    } else if (ln < 2 * N) {  // eta += HA^T S^-1 v
-      const int r = ln - N;
-      S s = eta[r];
-#pragma unroll
-      for (int q = 0; q < M; ++q) s = sfma(HCA[q * LDH + RF::HAO + r], AUG[q * LDA + M + 2 * N], s);
-      eta[r] = s;
+      eta[ln] = h;
     }
-    __syncwarp();
+    gsync();
   }
   const FOffs F(N);
   S* o = agg + c * F.size;
@@ -308,7 +304,7 @@ __device__ __forceinline__ void t_predict(S* fr, const S* mf, const S* P, S* Pn)
     if (ln < N)
       fr[FF::xp + ln] = mf[MF::u + ln] + matvec_row<N, N, 1, LD>(Fc, fr + FF::x, ln);
   }
-  __syncwarp();
+  gsync();
   {
     using P_ = Pick<N, N>;
     using TL = Tiling<N, N, P_::TM, P_::TN>;
@@ -321,7 +317,7 @@ __device__ __forceinline__ void t_predict(S* fr, const S* mf, const S* P, S* Pn)
       put<P_::TM, P_::TN, LD2, 1>(AUG2 + r0 * LD2 + c0, acc);
     }
   }
-  __syncwarp();
+  gsync();
 }
 
 // Smoothing element of step kp from its filtered (x, P) and the prediction
@@ -357,20 +353,20 @@ __device__ __forceinline__ void t_smooth_elem(S* fr, S* P, S*& Ea, S*& Eb, S* eg
       fr[FF::g + ln] = s;
     }
   }
-  __syncwarp();
+  gsync();
   // per-step element to global: E^T, g, L (SOffs sizes)
   const SOffs SO(N);
   gstore_mat<N, LD2, false, false>(eglk + SO.E, Et);
   if (ln < N) eglk[SO.g + ln] = fr[FF::g + ln];
   gstore_mat<N, LD, false, false>(eglk + SO.L, P);
   if (first) {
-    for (int i = ln; i < N * N; i += 32) {
+    for (int i = ln; i < N * N; i += kGW) {
       const int r = i / N, c = i % N;
       Ea[r * LD + c] = Et[r * LD2 + c];  // E_a column-major = E^T row-major
       La[r * LD + c] = P[r * LD + c];
     }
     if (ln < N) fr[FF::ga + ln] = fr[FF::g + ln];
-    __syncwarp();
+    gsync();
     return;
   }
   S* Tt = fr + FF::FPt;  // FP is dead: T = E_a L (column-major)
@@ -391,7 +387,7 @@ __device__ __forceinline__ void t_smooth_elem(S* fr, S* P, S*& Ea, S*& Eb, S* eg
       fr[FF::ga + ln] = s;
     }
   }
-  __syncwarp();
+  gsync();
   {
     using P_ = Pick<N, N>;
     using TL = Tiling<N, N, P_::TM, P_::TN>;
@@ -413,7 +409,7 @@ __device__ __forceinline__ void t_smooth_elem(S* fr, S* P, S*& Ea, S*& Eb, S* eg
     Ea = Eb;
     Eb = t;
   }
-  __syncwarp();
+  gsync();
 }
 
 // Kalman update of (x, P) with step-k measurement blocks (kalman_seq.hpp:58-99)
@@ -444,19 +440,19 @@ __device__ __forceinline__ void t_update(S* fr, const S* mf, S* P, const S* y, u
       AUG3[ln * LDA3 + M + N] = v;
     }
   }
-  __syncwarp();
+  gsync();
   {  // S = HP H^T + R
-    constexpr int TM = M >= 8 ? 2 : 1;
-    using TL = Tiling<M, M, TM, 1>;
+    using P_ = Pick<M, M>;
+    using TL = Tiling<M, M, P_::TM, P_::TN>;
     if (TL::active()) {
       const int r0 = TL::r0(), c0 = TL::c0();
-      S acc[TM][1];
-      init<TM, 1, LDR, 1>(acc, mf + MF::R + r0 * LDR + c0);
-      mma<N, TM, 1, LDP, 1, LDM, 1>(acc, HP + r0 * LDP, Ht + c0);
-      put_sym<TM, 1, LDA3>(AUG3, acc, r0, c0);
+      S acc[P_::TM][P_::TN];
+      init<P_::TM, P_::TN, LDR, 1>(acc, mf + MF::R + r0 * LDR + c0);
+      mma<N, P_::TM, P_::TN, LDP, 1, LDM, 1>(acc, HP + r0 * LDP, Ht + c0);
+      put_sym<P_::TM, P_::TN, LDA3>(AUG3, acc, r0, c0);
     }
   }
-  __syncwarp();
+  gsync();
   gj_spd<M, M + N + 1, LDA3>(AUG3, fr + FF::pv, e);  // [I | K^T | S^-1 v]
   {  // P -= K HP
     using P_ = Pick<N, N>;
@@ -475,14 +471,14 @@ __device__ __forceinline__ void t_update(S* fr, const S* mf, S* P, const S* y, u
       x[ln] = s;
     }
   }
-  __syncwarp();
+  gsync();
 }
 
 // finish: filter the chunk from the prefix of chunk c-1.  SMOOTH = false
 // writes the filtered stats; SMOOTH = true the per-step smoothing elements
 // and the chunk's smoother element (sagg, SOffs layout, E row-major).
 template <typename S, int N, int M, bool SMOOTH>
-__global__ void __launch_bounds__(32 * kTileWarps)
+__global__ void __launch_bounds__(kGW * kGroupsFinish)
     k_t_finish(ModelView<S> m, long long L, long long nchunks, const S* pre, S* mean, S* cov,
                S* sagg, S* egl, unsigned* err) {
   using FF = FFrame<S, N, M>;
@@ -491,7 +487,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
   const bool inv = time_invariant(m);
   S *fr, *mf;
   frames<S, N, M, FF::size>(m, inv, fr, mf);
-  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / kGW;
   if (c >= nchunks) return;
   const int ln = lane();
   unsigned e = 0;
@@ -509,11 +505,11 @@ __global__ void __launch_bounds__(32 * kTileWarps)
     sload_mat<N, LD, false>(P, Ps);
     if (ln < N) fr[FF::x + ln] = xs[ln];
   }
-  __syncwarp();
+  gsync();
   for (long long k = k0; k < k1; ++k) {
     if (!inv) {
       load_model<S, N, M>(mf, m, k);
-      __syncwarp();
+      gsync();
     }
     t_predict<S, N, M>(fr, mf, P, Pn);
     if constexpr (SMOOTH) {
@@ -525,7 +521,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
       Pn = t;
       if (ln < N) fr[FF::x + ln] = fr[FF::xp + ln];
     }
-    __syncwarp();
+    gsync();
     const S* yk = inv ? m.Y(k) : mf + MF::y;
     t_update<S, N, M>(fr, mf, P, yk, e);
     if constexpr (!SMOOTH) {
@@ -540,12 +536,12 @@ __global__ void __launch_bounds__(32 * kTileWarps)
       // a_T = (0, x_T, P_T) (kalman_elems.hpp:158-163)
       const SOffs SO2(N);
       S* eglk = egl + kl * SO2.size;
-      for (int i = ln; i < N * N; i += 32) eglk[SO2.E + i] = S(0);
+      for (int i = ln; i < N * N; i += kGW) eglk[SO2.E + i] = S(0);
       if (ln < N) eglk[SO2.g + ln] = fr[FF::x + ln];
       gstore_mat<N, LD, false, false>(eglk + SO2.L, P);
       S* La = fr + FF::La;
       if (first) {
-        for (int i = ln; i < N * N; i += 32) {
+        for (int i = ln; i < N * N; i += kGW) {
           const int r = i / N, cc = i % N;
           Ea[r * LD + cc] = S(0);
           La[r * LD + cc] = P[r * LD + cc];
@@ -571,7 +567,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
             fr[FF::ga + ln] = s;
           }
         }
-        __syncwarp();
+        gsync();
         {
           using P_ = Pick<N, N>;
           using TL = Tiling<N, N, P_::TM, P_::TN>;
@@ -583,14 +579,14 @@ __global__ void __launch_bounds__(32 * kTileWarps)
             put_sym<P_::TM, P_::TN, LD>(La, acc, r0, c0);
           }
         }
-        __syncwarp();
-        for (int i = ln; i < N * N; i += 32) Ea[(i / N) * LD + i % N] = S(0);
+        gsync();
+        for (int i = ln; i < N * N; i += kGW) Ea[(i / N) * LD + i % N] = S(0);
       }
-      __syncwarp();
+      gsync();
     } else {
       if (!inv) {
         load_model<S, N, M>(mf, m, k1, true);
-        __syncwarp();
+        gsync();
       }
       t_predict<S, N, M>(fr, mf, P, Pn);
       t_smooth_elem<S, N, M>(fr, P, Ea, Eb, egl + kl * SO.size, first, e);
@@ -606,14 +602,14 @@ __global__ void __launch_bounds__(32 * kTileWarps)
 // smoother finish: backwards over the chunk from the suffix of chunk c+1,
 // x_s(k) = E_k x_s(k+1) + g_k, P_s(k) = E_k P_s(k+1) E_k^T + L_k.
 template <typename S, int N>
-__global__ void __launch_bounds__(32 * kTileWarps)
+__global__ void __launch_bounds__(kGW * kGroupsSmooth)
     k_t_smoother_finish(long long T, long long L, long long nchunks, const S* suf,
                         const S* egl, S* mean, S* cov) {
   using SF = SFrame<S, N>;
   constexpr int LD = SF::LD;
   extern __shared__ __align__(16) unsigned char tsm[];
-  S* fr = reinterpret_cast<S*>(tsm) + (threadIdx.x >> 5) * SF::size;
-  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  S* fr = reinterpret_cast<S*>(tsm) + (threadIdx.x / kGW) * SF::size;
+  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / kGW;
   if (c >= nchunks) return;
   const int ln = lane();
   const long long k0 = c * L, k1 = min(k0 + L, T);
@@ -628,7 +624,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
     sload_mat<N, LD, false>(Ps, s1 + SO.L);
     if (ln < N) xs[ln] = s1[SO.g + ln];
   } else {  // the last step has E = 0: the incoming state is never used
-    for (int i = ln; i < N * N; i += 32) Ps[(i / N) * LD + i % N] = S(0);
+    for (int i = ln; i < N * N; i += kGW) Ps[(i / N) * LD + i % N] = S(0);
     if (ln < N) xs[ln] = S(0);
   }
   for (long long i = k1 - 1; i >= k0; --i) {
@@ -636,7 +632,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
     sload_mat<N, LD, false>(Et, ek + SO.E);
     sload_mat<N, LD, false>(Lk, ek + SO.L);
     if (ln < N) fr[SF::g + ln] = ek[SO.g + ln];
-    __syncwarp();
+    gsync();
     {
       using P_ = Pick<N, N>;
       using TL = Tiling<N, N, P_::TM, P_::TN>;
@@ -654,7 +650,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
         fr[SF::tmp + ln] = s;
       }
     }
-    __syncwarp();
+    gsync();
     {
       using P_ = Pick<N, N>;
       using TL = Tiling<N, N, P_::TM, P_::TN>;
@@ -667,7 +663,7 @@ __global__ void __launch_bounds__(32 * kTileWarps)
       }
       if (ln < N) xs[ln] = fr[SF::tmp + ln];
     }
-    __syncwarp();
+    gsync();
     if (ln < N) mean[i * N + ln] = xs[ln];
     gstore_mat<N, LD, false, true>(cov + i * N * N, Ps);
   }
@@ -681,15 +677,14 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
   const long long T = m.t;
   if (T == 0) return 0;
   const bool inv = time_invariant(m);
-  const int smem_r = cta_smem<S, N, M, RFrame<S, N, M>::size>(inv);
-  const int smem_f = cta_smem<S, N, M, FFrame<S, N, M>::size>(inv);
-  const int smem_s = (int)sizeof(S) * kTileWarps * SFrame<S, N>::size;
-  constexpr int block = 32 * kTileWarps;
+  const int smem_r = cta_smem<S, N, M, RFrame<S, N, M>::size, kGroupsReduce>(inv);
+  const int smem_f = cta_smem<S, N, M, FFrame<S, N, M>::size, kGroupsFinish>(inv);
+  const int smem_s = (int)sizeof(S) * kGroupsSmooth * SFrame<S, N>::size;
   long long Lc = a.chunk;
-  if (Lc < 1) {  // auto: `waves` (default 4) waves of co-resident finish warps
-    const int per_sm = kernel_setup(k_t_finish<S, N, M, true>, block, smem_f);
-    const long long resident =
-        (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kTileWarps * (a.waves > 0 ? a.waves : 4);
+  if (Lc < 1) {  // auto: `waves` (default 4) waves of co-resident finish groups
+    const int per_sm = kernel_setup(k_t_finish<S, N, M, true>, kGW * kGroupsFinish, smem_f);
+    const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
+                               kGroupsFinish * (a.waves > 0 ? a.waves : 4);
     Lc = (T + resident - 1) / resident;
     if (Lc < 1) Lc = 1;
   }
@@ -709,11 +704,12 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
   S* sagg = a.method == 1 ? (S*)alloc(sizeof(S) * SO.size * npad, actx) : nullptr;
   S* egl = a.method == 1 ? (S*)alloc(sizeof(S) * SO.size * T, actx) : nullptr;
   if (!agg || !aux1 || !aux2 || (a.method == 1 && (!sagg || !egl))) return 8;
-  const int grid = wide_blocks(nch, kTileWarps);
+  auto grid = [&](int g) { return wide_blocks(nch, g); };
   WideFilterOps<S> fops{L.err, N};
   WideSmootherOps<S> sops{N};
-  kernel_setup(k_t_reduce<S, N, M>, block, smem_r);
-  k_t_reduce<S, N, M><<<grid, block, smem_r, L.stream>>>(m, Lc, nch, agg, L.err);
+  constexpr int br = kGW * kGroupsReduce, bf = kGW * kGroupsFinish, bs = kGW * kGroupsSmooth;
+  kernel_setup(k_t_reduce<S, N, M>, br, smem_r);
+  k_t_reduce<S, N, M><<<grid(kGroupsReduce), br, smem_r, L.stream>>>(m, Lc, nch, agg, L.err);
   L.count("tile_filter_reduce");
   if (npad > nch) {
     k_wide_fill_identity<<<wide_blocks(npad - nch, 4), 128, 0, L.stream>>>(
@@ -722,15 +718,15 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
   }
   if (npad > 1) wide_scan(L, fops, agg, npad, aux1, aux2, plan, 0);
   if (a.method == 0) {
-    kernel_setup(k_t_finish<S, N, M, false>, block, smem_f);
-    k_t_finish<S, N, M, false><<<grid, block, smem_f, L.stream>>>(m, Lc, nch, agg, mean, cov,
-                                                                 nullptr, nullptr, L.err);
+    kernel_setup(k_t_finish<S, N, M, false>, bf, smem_f);
+    k_t_finish<S, N, M, false><<<grid(kGroupsFinish), bf, smem_f, L.stream>>>(
+        m, Lc, nch, agg, mean, cov, nullptr, nullptr, L.err);
     L.count("tile_filter_finish");
     return 0;
   }
-  kernel_setup(k_t_finish<S, N, M, true>, block, smem_f);
-  k_t_finish<S, N, M, true><<<grid, block, smem_f, L.stream>>>(m, Lc, nch, agg, mean, cov, sagg,
-                                                              egl, L.err);
+  kernel_setup(k_t_finish<S, N, M, true>, bf, smem_f);
+  k_t_finish<S, N, M, true><<<grid(kGroupsFinish), bf, smem_f, L.stream>>>(
+      m, Lc, nch, agg, mean, cov, sagg, egl, L.err);
   L.count("tile_filter_finish_smoother_reduce");
   if (npad > nch) {
     k_wide_fill_identity<<<wide_blocks(npad - nch, 4), 128, 0, L.stream>>>(
@@ -738,8 +734,9 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
     L.count("fill_identity");
   }
   if (npad > 1) wide_scan(L, sops, sagg, npad, aux1, aux2, plan, 1);
-  kernel_setup(k_t_smoother_finish<S, N>, block, smem_s);
-  k_t_smoother_finish<S, N><<<grid, block, smem_s, L.stream>>>(T, Lc, nch, sagg, egl, mean, cov);
+  kernel_setup(k_t_smoother_finish<S, N>, bs, smem_s);
+  k_t_smoother_finish<S, N><<<grid(kGroupsSmooth), bs, smem_s, L.stream>>>(T, Lc, nch, sagg, egl,
+                                                                          mean, cov);
   L.count("tile_smoother_finish");
   return 0;
 }
