@@ -240,6 +240,77 @@ __device__ __forceinline__ void gj_spd(S* X, S* pv, unsigned& err) {
   gsync();
 }
 
+// Gauss-Jordan elimination WITH partial pivoting (the reference's pivoted LU,
+// mat.hpp:180-205: first maximum |a(r, p)| over r >= p) on the R x W block
+// X: [A | B] -> [I | A^-1 B] for a general nonsingular A (a zero pivot
+// raises kErrSingular).  Same layout as gj_spd; the pivot row is found by the
+// owner of column p and broadcast to the group with a shuffle, and every lane
+// swaps rows p and pr of its columns in registers (predicated, static
+// indices).
+template <int R, int W, int LDX, typename S>
+__device__ __forceinline__ void gj_piv(S* X, S* pv, unsigned& err) {
+  constexpr int NC = (W + kGW - 1) / kGW;
+  static_assert(R <= kGW, "pivot column owner");
+  const int ln = lane();
+  const int base = threadIdx.x & 31 & ~(kGW - 1);
+  S x[NC][R];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = ln + kGW * c;
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[c][i] = col < W ? X[i * LDX + col] : S(0);
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    S best = S(-1);
+    int pr = p;
+#pragma unroll
+    for (int i = p; i < R; ++i)
+      if (sabs(x[0][i]) > best) {
+        best = sabs(x[0][i]);
+        pr = i;
+      }
+    pr = __shfl_sync(gmask(), pr, base + p);
+    if (pr != p) {  // group-uniform: swap rows p and pr in every column
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const S a = x[c][p];
+#pragma unroll
+        for (int i = p + 1; i < R; ++i)
+          if (i == pr) {
+            x[c][p] = x[c][i];
+            x[c][i] = a;
+          }
+      }
+    }
+    S* buf = pv + (p & 1) * R;
+    if (ln == p) st<R, 1>(buf, x[0]);
+    gsync();
+    S col[R];
+    ld<R, 1>(col, buf);
+    const S d = col[p];
+    if (d == S(0)) err |= kErrSingular;
+    const S ip = srcp(d);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const S rp = x[c][p] * ip;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i != p) x[c][i] = sfma(-col[i], rp, x[c][i]);
+      x[c][p] = rp;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = ln + kGW * c;
+    if (col < W) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) X[i * LDX + col] = x[c][i];
+    }
+  }
+  gsync();
+}
+
 // y(r) = sum_k A(r, k) x(k) (+ z(r)), A(r, k) at a[r AR + k AK]; lanes r < n
 template <int n, int K, int AR, int AK, typename S>
 __device__ __forceinline__ S matvec_row(const S* a, const S* x, int r) {

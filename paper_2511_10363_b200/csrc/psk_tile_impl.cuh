@@ -669,6 +669,267 @@ __global__ void __launch_bounds__(kGW * kGroupsSmooth)
   }
 }
 
+// ---- PTFS backward pass -------------------------------------------------------
+template <typename S, int N, int M>
+struct BFrame {  // backward finish
+  static constexpr int V = vec16<S>();
+  static constexpr int LD = ldpad<S>(N), MAT = N * LD;
+  static constexpr int HAO = N + V, LDH = ldpad<S>(HAO + N), LDA = ldpad<S>(M + 2 * N + 1);
+  static constexpr int LDG = ldpad<S>(2 * N + 1);  // [N | J A | w] and [M | P | rhs]
+  static constexpr int J = 0, Aa = MAT, Ca = 2 * MAT + V, P = 3 * MAT + 2 * V,
+                       Ja = 4 * MAT + 2 * V, HCA = 5 * MAT + 2 * V, AUG = HCA + M * LDH,
+                       G = AUG + M * LDA,
+                       eta = G + N * LDG, etaa = eta + up16<S>(N), ba = etaa + up16<S>(N),
+                       x = ba + up16<S>(N), vv = x + up16<S>(N), pv = vv + up16<S>(M),
+                       size = pv + 2 * up16<S>(N > M ? N : M);
+};
+constexpr int kGroupsBwd = 4;
+
+// The backward pass of the two-filter smoother (Alg. 7, kalman_par.hpp:
+// 183-238) for chunk c, walking its slots backwards: slot i holds the filter
+// element of step i+1 (`ms` is the model shifted by one step; no element past
+// the series' last transition, build_shifted_filter_elems kalman_par.hpp:
+// 63-89).  The running backward information (eta, J) starts from the
+// reverse-scanned suffix of chunk c+1; at each slot it becomes the eta / J
+// rows of a (x) (eta, J) (Lemma 1, kalman_elems.hpp:267-336, with the element
+// built from the identity by the conditional-Kalman update), then the
+// two-filter combination (kalman_seq.hpp:239-260) turns the filtered (x, P)
+// of step i -- read from mean / cov -- into the smoothed stats, written in
+// place.  Both non-symmetric solves are pivoted Gauss-Jordan eliminations.
+template <typename S, int N, int M>
+__global__ void __launch_bounds__(kGW * kGroupsBwd)
+    k_t_bwd_finish(ModelView<S> ms, long long T, long long L, long long nchunks, const S* suf,
+                   S* mean, S* cov, unsigned* err) {
+  using BF = BFrame<S, N, M>;
+  using MF = ModelFrame<S, N, M>;
+  constexpr int LD = BF::LD, LDH = BF::LDH, LDA = BF::LDA, LDG = BF::LDG, LDM = MF::LDM,
+                LDR = MF::LDR;
+  const bool inv = time_invariant(ms);
+  S *fr, *mf;
+  frames<S, N, M, BF::size>(ms, inv, fr, mf);
+  const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / kGW;
+  if (c >= nchunks) return;
+  const int ln = lane();
+  unsigned e = 0;
+  const long long k0 = c * L, k1 = min(k0 + L, T);
+  const FOffs FO(N);
+  S* J = fr + BF::J;
+  S* Aa = fr + BF::Aa;
+  S* Ca = fr + BF::Ca;
+  S* P = fr + BF::P;
+  S* Ja = fr + BF::Ja;
+  S* HCA = fr + BF::HCA;
+  S* AUG = fr + BF::AUG;
+  S* G = fr + BF::G;
+  S* eta = fr + BF::eta;
+  S* etaa = fr + BF::etaa;
+  S* ba = fr + BF::ba;
+  S* x = fr + BF::x;
+  S* vv = fr + BF::vv;
+  S* pv = fr + BF::pv;
+  const S* Fc = mf + MF::Fc;
+  const S* Qm = mf + MF::Q;
+  const S* Ht = mf + MF::Ht;
+  const S* Rm = mf + MF::R;
+  if (c + 1 < nchunks) {  // the suffix of the later chunks
+    const S* s1 = suf + (c + 1) * FO.size;
+    sload_mat<N, LD, false>(J, s1 + FO.J);
+    if (ln < N) eta[ln] = s1[FO.eta + ln];
+  } else {
+    for (int i = ln; i < N * N; i += kGW) J[(i / N) * LD + i % N] = S(0);
+    if (ln < N) eta[ln] = S(0);
+  }
+  gsync();
+  // A time-invariant model has the same element matrices (A_a, C_a, J_a and
+  // the gain) at every slot; only b_a and eta_a follow y.  They are built
+  // once per chunk, and each slot then costs three matrix-vector products.
+  bool built = false;
+  for (long long i = k1 - 1; i >= k0; --i) {
+    if (i < ms.t && inv && built) {
+      if (ln < M) {  // v = y - H u - d
+        const S v = ms.Y(i)[ln] - mf[MF::d + ln] - matvec_row<M, N, 1, LDM>(Ht, mf + MF::u, ln);
+        vv[ln] = v;
+      }
+      gsync();
+      if (ln < N) {  // b_a = u + K v, eta_a = (S^-1 HA)^T v
+        S b = mf[MF::u + ln], h = S(0);
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          b = sfma(AUG[q * LDA + M + ln], vv[q], b);
+          h = sfma(AUG[q * LDA + M + N + ln], vv[q], h);
+        }
+        ba[ln] = b;
+        etaa[ln] = h;
+      }
+      gsync();
+    } else if (i < ms.t) {  // slot i holds the element of step i+1
+      if (!inv) {
+        load_model<S, N, M>(mf, ms, i);
+        gsync();
+      }
+      built = true;
+      // the element from the identity: A = F, b = u, C = Q, updated with y
+      {  // [HC | HA] = H [Q | F]
+        using P_ = Pick<M, 2 * N>;
+        using TL = Tiling<M, 2 * N, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          zero(acc);
+          if (c0 < N)
+            mma<N, P_::TM, P_::TN, 1, LDM, LD, 1>(acc, Ht + r0, Qm + c0);
+          else  // F(k, c) = Fc[c LD + k]
+            mma<N, P_::TM, P_::TN, 1, LDM, 1, LD>(acc, Ht + r0, Fc + (c0 - N) * LD);
+          put<P_::TM, P_::TN, LDH, 1>(HCA + r0 * LDH + (c0 < N ? c0 : c0 - N + BF::HAO), acc);
+          put<P_::TM, P_::TN, LDA, 1>(AUG + r0 * LDA + M + c0, acc);
+        }
+        if (ln < M) {  // v = y - H u - d
+          const S y = inv ? ms.Y(i)[ln] : mf[MF::y + ln];
+          const S v = y - mf[MF::d + ln] - matvec_row<M, N, 1, LDM>(Ht, mf + MF::u, ln);
+          vv[ln] = v;
+          AUG[ln * LDA + M + 2 * N] = v;
+        }
+      }
+      gsync();
+      {  // S = HC H^T + R
+        using P_ = Pick<M, M>;
+        using TL = Tiling<M, M, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          init<P_::TM, P_::TN, LDR, 1>(acc, Rm + r0 * LDR + c0);
+          mma<N, P_::TM, P_::TN, LDH, 1, LDM, 1>(acc, HCA + r0 * LDH, Ht + c0);
+          put_sym<P_::TM, P_::TN, LDA>(AUG, acc, r0, c0);
+        }
+      }
+      gsync();
+      gj_spd<M, M + 2 * N + 1, LDA>(AUG, pv, e);  // [I | K^T | S^-1 HA | S^-1 v]
+      {  // J_a = HA^T S^-1 HA
+        using P_ = Pick<N, N>;
+        using TL = Tiling<N, N, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          zero(acc);
+          mma<M, P_::TM, P_::TN, 1, LDH, LDA, 1>(acc, HCA + BF::HAO + r0, AUG + M + N + c0);
+          put_sym<P_::TM, P_::TN, LD>(Ja, acc, r0, c0);
+        }
+      }
+      {  // [A_a | C_a] = [F | Q] - K [HA | HC]
+        using P_ = Pick<N, 2 * N>;
+        using TL = Tiling<N, 2 * N, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          const bool left = c0 < N;
+          if (left)
+            init<P_::TM, P_::TN, 1, LD>(acc, Fc + c0 * LD + r0);  // F(r, c) = Fc[c LD + r]
+          else
+            init<P_::TM, P_::TN, LD, 1>(acc, Qm + r0 * LD + (c0 - N));
+          const S* rp = left ? HCA + BF::HAO + c0 : HCA + (c0 - N);
+          mma<M, P_::TM, P_::TN, 1, LDA, LDH, 1, true>(acc, AUG + M + r0, rp);
+          if (left)
+            put<P_::TM, P_::TN, LD, 1>(Aa + r0 * LD + c0, acc);
+          else
+            put_sym<P_::TM, P_::TN, LD>(Ca, acc, r0, c0 - N);
+        }
+      }
+      if (ln < N) {  // b_a = u + K v, eta_a = HA^T S^-1 v
+        S b = mf[MF::u + ln], h = S(0);
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          b = sfma(AUG[q * LDA + M + ln], vv[q], b);
+          h = sfma(HCA[q * LDH + BF::HAO + ln], AUG[q * LDA + M + 2 * N], h);
+        }
+        ba[ln] = b;
+        etaa[ln] = h;
+      }
+      gsync();
+    }
+    if (i < ms.t) {
+      // (eta, J) <- a (x) (eta, J): G = [I + J C_a | J A_a | eta - J b_a]
+      {
+        using P_ = Pick<N, 2 * N>;
+        using TL = Tiling<N, 2 * N, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          zero(acc);
+          const bool left = c0 < N;
+          mma<N, P_::TM, P_::TN, 1, LD, LD, 1>(acc, J + r0, left ? Ca + c0 : Aa + (c0 - N));
+          if (left) {
+#pragma unroll
+            for (int a = 0; a < P_::TM; ++a)
+#pragma unroll
+              for (int b = 0; b < P_::TN; ++b)
+                if (r0 + a == c0 + b) acc[a][b] += S(1);
+          }
+          put<P_::TM, P_::TN, LDG, 1>(G + r0 * LDG + c0, acc);
+        }
+        if (ln < N) {
+          S w = eta[ln];
+#pragma unroll
+          for (int q = 0; q < N; ++q) w = sfma(-J[ln * LD + q], ba[q], w);
+          G[ln * LDG + 2 * N] = w;
+        }
+      }
+      gsync();
+      gj_piv<N, 2 * N + 1, LDG>(G, pv, e);  // [I | N^-1 J A_a | N^-1 w]
+      {  // J = A_a^T (N^-1 J A_a) + J_a ; eta = A_a^T N^-1 w + eta_a
+        using P_ = Pick<N, N>;
+        using TL = Tiling<N, N, P_::TM, P_::TN>;
+        if (TL::active()) {
+          const int r0 = TL::r0(), c0 = TL::c0();
+          S acc[P_::TM][P_::TN];
+          init<P_::TM, P_::TN, LD, 1>(acc, Ja + r0 * LD + c0);
+          mma<N, P_::TM, P_::TN, 1, LD, LDG, 1>(acc, Aa + r0, G + N + c0);
+          put_sym<P_::TM, P_::TN, LD>(J, acc, r0, c0);
+        }
+        if (ln < N) {
+          S h = etaa[ln];
+#pragma unroll
+          for (int q = 0; q < N; ++q) h = sfma(Aa[q * LD + ln], G[q * LDG + 2 * N], h);
+          eta[ln] = h;
+        }
+      }
+      gsync();
+    }
+    // two-filter combination with the filtered (x, P) of step i
+    sload_mat<N, LD, false>(P, cov + i * N * N);
+    if (ln < N) x[ln] = mean[i * N + ln];
+    gsync();
+    {  // G = [I + P J | P | x + P eta]
+      using P_ = Pick<N, N>;
+      using TL = Tiling<N, N, P_::TM, P_::TN>;
+      if (TL::active()) {
+        const int r0 = TL::r0(), c0 = TL::c0();
+        S acc[P_::TM][P_::TN];
+        zero(acc);
+        mma<N, P_::TM, P_::TN, 1, LD, LD, 1>(acc, P + r0, J + c0);
+#pragma unroll
+        for (int a = 0; a < P_::TM; ++a)
+#pragma unroll
+          for (int b = 0; b < P_::TN; ++b)
+            if (r0 + a == c0 + b) acc[a][b] += S(1);
+        put<P_::TM, P_::TN, LDG, 1>(G + r0 * LDG + c0, acc);
+      }
+      if (ln < N) {
+        S r = x[ln];
+#pragma unroll
+        for (int q = 0; q < N; ++q) r = sfma(P[ln * LD + q], eta[q], r);
+        G[ln * LDG + 2 * N] = r;
+      }
+      for (int k = ln; k < N * N; k += kGW) G[(k / N) * LDG + N + k % N] = P[(k / N) * LD + k % N];
+    }
+    gsync();
+    gj_piv<N, 2 * N + 1, LDG>(G, pv, e);  // [I | P_s | x_s]
+    if (ln < N) mean[i * N + ln] = G[ln * LDG + 2 * N];
+    gstore_mat<N, LDG, false, true>(cov + i * N * N, G + N);
+    gsync();
+  }
+  if (e && ln == 0) atomicOr(err, e);
+}
+
 // ---- host dispatch --------------------------------------------------------------
 template <typename S, int N, int M>
 int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
@@ -717,11 +978,39 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
     L.count("fill_identity");
   }
   if (npad > 1) wide_scan(L, fops, agg, npad, aux1, aux2, plan, 0);
-  if (a.method == 0) {
+  if (a.method == 0 || a.method == 2) {
     kernel_setup(k_t_finish<S, N, M, false>, bf, smem_f);
     k_t_finish<S, N, M, false><<<grid(kGroupsFinish), bf, smem_f, L.stream>>>(
         m, Lc, nch, agg, mean, cov, nullptr, nullptr, L.err);
     L.count("tile_filter_finish");
+    if (a.method == 0) return 0;
+    // PTFS backward pass: shifted elements (slot i = step i+1) reduced per
+    // chunk from the identity, reverse scan, backward finish fused with the
+    // two-filter combination over the filtered stats in mean / cov
+    ModelView<S> ms = m;
+    ms.f += m.sf; ms.u += m.su; ms.q += m.sq; ms.h += m.sh; ms.d += m.sd; ms.r += m.sr;
+    ms.y += m.sy;
+    ms.t = T - 1;
+    ms.prior_first = 0;
+    ms.last_step = ms.t - 1;
+    const long long nch_s = ms.t > 0 ? (ms.t + Lc - 1) / Lc : 0;
+    if (nch_s > 0) {
+      k_t_reduce<S, N, M><<<wide_blocks(nch_s, kGroupsReduce), br, smem_r, L.stream>>>(
+          ms, Lc, nch_s, agg, L.err);
+      L.count("tile_bwd_reduce");
+    }
+    if (npad > nch_s) {
+      k_wide_fill_identity<<<wide_blocks(npad - nch_s, 4), 128, 0, L.stream>>>(
+          fops, ElemBuf<S>{agg, npad, npad, 0}, nch_s, npad);
+      L.count("fill_identity");
+    }
+    if (npad > 1) wide_scan(L, fops, agg, npad, aux1, aux2, plan, 1);
+    const int smem_b = cta_smem<S, N, M, BFrame<S, N, M>::size, kGroupsBwd>(inv);
+    constexpr int bb = kGW * kGroupsBwd;
+    kernel_setup(k_t_bwd_finish<S, N, M>, bb, smem_b);
+    k_t_bwd_finish<S, N, M><<<grid(kGroupsBwd), bb, smem_b, L.stream>>>(ms, T, Lc, nch, agg, mean,
+                                                                     cov, L.err);
+    L.count("tile_bwd_finish_tf_combine");
     return 0;
   }
   kernel_setup(k_t_finish<S, N, M, true>, bf, smem_f);
@@ -747,7 +1036,7 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
 template <typename S>
 int tile_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, S* cov,
              void* (*alloc)(size_t, void*), void* actx) {
-  if (a.method == 2 || !m.prior_first || m.last_step != m.t - 1) return -1;
+  if (!m.prior_first || m.last_step != m.t - 1) return -1;
 #define PSK_CASE(A, B) \
   if (m.nx == A && m.ny == B) return tile_run_t<S, A, B>(L, m, a, mean, cov, alloc, actx);
   PSK_TILE_DIMS(PSK_CASE)

@@ -135,3 +135,31 @@ def test_config5_subset_2p20_f64(psk, gpu, port):
     for b, o, r in zip(picks, outs, refs):
         e = max_rel_err(o.mean, o.cov, *r)
         assert e < TOL64, (b, e)
+
+
+def test_config5_ptfs_and_pkf_tiled(psk, gpu, port):
+    """The two-filter smoother and the filter at nx = 16, ny = 8 through the
+    register-tiled kernels (PTFS backward pass fused with the two-filter
+    combination), one configs[4] series at T = 2^17, vs the sequential
+    oracle; the runtime-dimension kernels (option "tile" = 0) agree."""
+    t = 1 << 17
+    m, ys = _config5_series(port, psk, 5, t)
+    with ThreadPoolExecutor(2) as ex:
+        rts = ex.submit(port.rts_run, m, ys)
+        kf = ex.submit(port.kf_run, m, ys)
+        rts, kf = rts.result(), kf.result()
+    be = psk.CudaBackend(gpu)
+    spec = psk.ScanSpec(psk.ScanAlg.DecoupledLookback)
+    be.set_profile(True)
+    got = psk.ptfs_run(m, ys, spec, be)
+    assert any(n == "tile_bwd_finish_tf_combine" for n, _ in be.last_profile())
+    e = max_rel_err(got.mean, got.cov, *rts)
+    assert e < TOL64, e
+    got = psk.pkf_run(m, ys, spec, be)
+    e = max_rel_err(got.mean, got.cov, *kf)
+    assert e < TOL64, e
+    wide = psk.CudaBackend(gpu)
+    wide.set_option("tile", 0)
+    w = psk.prts_run(m, ys, spec, wide)
+    got = psk.prts_run(m, ys, spec, be)
+    assert max_rel_err(got.mean, got.cov, w.mean, w.cov) < 1e-10
