@@ -1,0 +1,8 @@
+"""One-line summary of a bench.py JSON line on stdin (A/B sweeps):
+label, dtype, ms/step, per-kernel average ms."""
+import json
+import sys
+
+d = json.loads(sys.stdin.read().strip().splitlines()[-1])
+print(sys.argv[1] if len(sys.argv) > 1 else "", d["dtype"], round(d["ms_per_step"], 3),
+      {k: v["avg_ms"] for k, v in d["kernels"].items()}, flush=True)

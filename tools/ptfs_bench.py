@@ -4,7 +4,9 @@ nx = 4, ny = 2, FP64, device-resident): PTFS on one context vs forward and
 backward passes on two contexts (devices = 2: two GPUs when more than one is
 visible, else two streams of one GPU), next to PRTS.  CUDA events around the
 synchronous calls (the two-context call spans both devices, so its time is
-taken on the forward device after both finished).  Prints JSON lines.
+taken on the forward device after both finished); the multi-device context
+(psk_create_multi over all visible GPUs, or two streams of GPU 0) runs the
+two filters on its halves.  Prints JSON lines.
 """
 from __future__ import annotations
 
@@ -42,9 +44,15 @@ def main() -> None:
     fwd = psk.CudaBackend(0)
     bwd = psk.CudaBackend(1 if ngpu > 1 else 0)
     spec = psk.ScanSpec(psk.ScanAlg.DecoupledLookback)
+    # a multi-device context (psk_create_multi): the two filters on its two
+    # halves, each time-sharded when the halves have several devices
+    devs = list(range(min(ngpu, 8))) if ngpu > 1 else [0, 0]
+    multi = psk.CudaBackend(devs)
     runs = {"prts": lambda: psk.prts_run(m, ys, spec, fwd),
             "ptfs_1ctx": lambda: psk.ptfs_run(m, ys, spec, fwd),
-            "ptfs_2ctx": lambda: psk.ptfs_run(m, ys, spec, fwd, bwd, 2)}
+            "ptfs_2ctx": lambda: psk.ptfs_run(m, ys, spec, fwd, bwd, 2),
+            "ptfs_multi": lambda: psk.ptfs_run(m, ys, spec, multi, multi, len(devs)),
+            "prts_multi": lambda: psk.prts_run(m, ys, spec, multi)}
     for name, fn in runs.items():
         for _ in range(3):
             fn()
@@ -60,6 +68,7 @@ def main() -> None:
         ms = e0.elapsed_time(e1) / reps
         print(json.dumps({"config": f"T=2^{log2t} nx=4 ny=2 f64", "run": name,
                           "bwd_device": bwd.device if name == "ptfs_2ctx" else None,
+                          "devices": devs if name.endswith("multi") else None,
                           "ms": round(ms, 4), "steps_per_s": T / (ms * 1e-3)}), flush=True)
 
 
