@@ -350,6 +350,10 @@ def run_psk(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test rig only (tests/test_gpu_bench_ranks.py): all ranks on one GPU over
+    # gloo, to exercise the N > 1 path where NCCL refuses two ranks per GPU
+    local = int(os.environ.get("PSK_BENCH_DEVICE", local))
+    backend = os.environ.get("PSK_BENCH_DIST_BACKEND", "nccl")
     if world != args.gpus and rank == 0:
         print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -357,7 +361,10 @@ def run_psk(args) -> None:
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist.group.WORLD
     T = 1 << args.log2t
     f64 = args.dtype == "f64"
