@@ -77,7 +77,7 @@ def _traffic(kernel: str, log2t: int, dtype: str, chunk: int) -> tuple:
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled (NVML, ~1 kHz) during the timed
+    """SM clocks and throttle reasons sampled (NVML, every 5 ms) during the timed
     region; falls back to nvidia-smi polling when NVML is unavailable."""
 
     REASONS = {  # nvmlClocksEventReason bits
@@ -119,7 +119,9 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.001)
+            # 5 ms: NVML queries contend with the CUDA driver; polling at 1 kHz
+            # stalled the host's kernel launches by milliseconds now and then
+            time.sleep(0.005)
 
     def __exit__(self, *a):
         self._stop.set()
