@@ -185,3 +185,38 @@ def test_multi_device_batch_and_fallbacks(gpu, port):
     m, ys = gen(port, 71, 4, 2, 1)
     got = psk.prts_run(m, ys, psk.ScanSpec(psk.ScanAlg.InplaceLaFi), be)
     assert max_rel_err(got.mean, got.cov, *port.rts_run(m, ys)) < 1e-9
+
+
+def test_multi_device_f32_and_short_series(gpu, port):
+    """FP32 through a multi-device context on the stationary tracking model
+    (FP32 gate 1e-4 vs the f64 oracle), and series shorter than the member
+    count (one member runs them)."""
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200.synthetic import cv_model
+    m64, ys64 = cv_model(1 << 15, seed=8)
+    m32, ys32 = cv_model(1 << 15, seed=8, dtype=np.float32)
+    rts = port.rts_run(m64, ys64)
+    be = psk.CudaBackend([0, 0, 0, 0])
+    spec = psk.ScanSpec(psk.ScanAlg.DecoupledLookback)
+    got = psk.prts_run(m32, ys32, spec, be)
+    assert max_rel_err(got.mean, got.cov, *rts) < 1e-4
+    got = psk.ptfs_run(m32, ys32, spec, be, be, 4)
+    assert max_rel_err(got.mean, got.cov, *rts) < 1e-4
+    be8 = psk.CudaBackend([0] * 8)
+    for t in (2, 5, 9):
+        m, ys = gen(port, 80 + t, 4, 2, t)
+        ref = port.rts_run(m, ys)
+        got = psk.prts_run(m, ys, spec, be8)
+        assert max_rel_err(got.mean, got.cov, *ref) < 1e-9, t
+        got = psk.ptfs_run(m, ys, spec, be8, be8, 8)
+        assert max_rel_err(got.mean, got.cov, *ref) < 1e-9, t
+
+
+def test_virtual_sharded_ptfs_f32(gpu, port):
+    import paper_2511_10363_b200 as psk
+    from paper_2511_10363_b200.synthetic import cv_model
+    m64, ys64 = cv_model(1 << 16, seed=12)
+    m32, ys32 = cv_model(1 << 16, seed=12, dtype=np.float32)
+    rts = port.rts_run(m64, ys64)
+    mean, cov = _virtual_sharded_ptfs(psk, m32, ys32, 3, 0, 6, gpu)
+    assert max_rel_err(mean, cov, *rts) < 1e-4
