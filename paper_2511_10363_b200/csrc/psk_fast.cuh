@@ -525,13 +525,18 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
     g2 |= (maps.grp[f] == 2 ? 1u : 0u) << f;
     g4 |= (maps.grp[f] == 4 ? 1u : 0u) << f;
   }
+  // row of walk position j in field f's box: j / grp, grp in {1, 2, 4} -- a
+  // shift (a 64-bit division here was a ~100-instruction call per field per
+  // step on the issuing thread, which the whole CTA then waited for at the
+  // step barrier)
+  auto grp_shift = [&](int f) { return (int)((g2 >> f) & 1u) + 2 * (int)((g4 >> f) & 1u); };
   auto issue = [&](int s, long long j) {
     fence_proxy_async();  // generic reads of this stage (last use) before the refill
     mbar_expect_tx(&bars[s], maps.tx);
 #pragma unroll
     for (int f = 0; f < 7; ++f)
       if (maps.use[f])
-        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)(j / maps.grp[f]),
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j >> grp_shift(f),
                     (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {
@@ -584,13 +589,14 @@ __device__ __forceinline__ void staged_walk_rev(unsigned char* smem_raw, const S
   // positions >= the m-length of the CTA's first chunk carry no data; the
   // i-th fetch is position jd - 1 - i
   const long long jd = min(jn, max(0LL, m.t - cta0 * L));
+  auto grp_shift = [&](int f) { return (int)((g2 >> f) & 1u) + 2 * (int)((g4 >> f) & 1u); };
   auto issue = [&](int s, long long j) {
     fence_proxy_async();
     mbar_expect_tx(&bars[s], maps.tx);
 #pragma unroll
     for (int f = 0; f < 7; ++f)
       if (maps.use[f])
-        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)(j / maps.grp[f]),
+        tma_load_3d(sm + s * In::stage + In::off(f), &maps.m[f], 0, (int)j >> grp_shift(f),
                     (int)cta0, &bars[s]);
   };
   if (tma && t == 0) {

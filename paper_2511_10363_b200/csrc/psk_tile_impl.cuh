@@ -50,9 +50,12 @@ struct RFrame {  // reduce
   static constexpr int LD = ldpad<S>(N), MAT = N * LD;
   static constexpr int HAO = N + V;  // column of HA inside an HCA row
   static constexpr int LDH = ldpad<S>(HAO + N), LDA = ldpad<S>(M + 2 * N + 1);
-  static constexpr int A0 = 0, A1 = MAT, C = 2 * MAT + V, T = 3 * MAT + 2 * V,
-                       J = 4 * MAT + 2 * V, HCA = 5 * MAT + 2 * V,
-                       AUG = HCA + M * LDH, b = AUG + M * LDA, eta = b + up16<S>(N),
+  // T (F C, column-major) is live from the prediction to C's update only, the
+  // measurement blocks HCA / AUG after it: they share one region
+  static constexpr int A0 = 0, A1 = MAT, C = 2 * MAT + V, J = 3 * MAT + 2 * V,
+                       T = 4 * MAT + 2 * V, HCA = T, AUG = HCA + M * LDH,
+                       REnd = (AUG + M * LDA > T + MAT) ? AUG + M * LDA : T + MAT,
+                       b = REnd, eta = b + up16<S>(N),
                        tmp = eta + up16<S>(N), vv = tmp + up16<S>(N), pv = vv + up16<S>(M),
                        size = pv + 2 * up16<S>(N > M ? N : M);
 };
@@ -60,9 +63,14 @@ template <typename S, int N, int M>
 struct FFrame {  // finish
   static constexpr int LD = ldpad<S>(N), MAT = N * LD;
   static constexpr int LD2 = ldpad<S>(2 * N), LDP = ldpad<S>(N), LDA3 = ldpad<S>(M + N + 1);
-  static constexpr int P0 = 0, P1 = MAT, FPt = 2 * MAT, Ea0 = 3 * MAT, Ea1 = 4 * MAT, La = 5 * MAT,
-                       AUG2 = 6 * MAT, HP = AUG2 + N * LD2, AUG3 = HP + M * LDP,
-                       x = AUG3 + M * LDA3, xp = x + up16<S>(N), g = xp + up16<S>(N),
+  // FP (column-major; later the fold's T = E_a L) is dead before the update's
+  // HP / [S | HP | v] blocks are formed: they share one region.  Three slots
+  // rotate between the filtered P, the predicted PP and the chunk's E_a.
+  static constexpr int P0 = 0, P1 = MAT, Ea0 = 2 * MAT, FPt = 3 * MAT, HP = FPt,
+                       AUG3 = HP + M * LDP,
+                       REnd = (AUG3 + M * LDA3 > FPt + MAT) ? AUG3 + M * LDA3 : FPt + MAT,
+                       La = REnd, AUG2 = La + MAT,
+                       x = AUG2 + N * LD2, xp = x + up16<S>(N), g = xp + up16<S>(N),
                        ga = g + up16<S>(N), vv = ga + up16<S>(N), pv = vv + up16<S>(M),
                        size = pv + 2 * up16<S>(N > M ? N : M);
 };
@@ -75,7 +83,7 @@ struct SFrame {  // smoother finish
 
 // chunks (lane groups) per CTA of each kernel: two CTAs per SM fit in shared
 // memory (reduce 12, finish 8, smoother finish 16 chunks per SM)
-constexpr int kGroupsReduce = 6, kGroupsFinish = 4, kGroupsSmooth = 8;
+constexpr int kGroupsReduce = 7, kGroupsFinish = 6, kGroupsSmooth = 8;
 
 template <typename S, int N, int M, int FR, int G>
 __host__ __device__ constexpr int cta_smem(bool invariant) {
@@ -326,7 +334,7 @@ __device__ __forceinline__ void t_predict(S* fr, const S* mf, const S* P, S* Pn)
 // folded into the chunk element (E_a column-major in *Ea, g_a, L_a):
 // E_a' = E_a E, g_a' = E_a g + g_a, L_a' = E_a L E_a^T + L_a.
 template <typename S, int N, int M>
-__device__ __forceinline__ void t_smooth_elem(S* fr, S* P, S*& Ea, S*& Eb, S* eglk, bool first,
+__device__ __forceinline__ void t_smooth_elem(S* fr, S*& P, S*& Ea, S* eglk, bool first,
                                               unsigned& e) {
   using FF = FFrame<S, N, M>;
   constexpr int LD = FF::LD, LD2 = FF::LD2;
@@ -398,16 +406,17 @@ __device__ __forceinline__ void t_smooth_elem(S* fr, S* P, S*& Ea, S*& Eb, S* eg
       init<P_::TM, P_::TN, LD, 1>(acc, La + r0 * LD + c0);
       mma<N, P_::TM, P_::TN, 1, LD, LD, 1>(acc, Tt + r0, Ea + c0);
       put_sym<P_::TM, P_::TN, LD>(La, acc, r0, c0);
-      // (E_a E)^T = E^T E_a^T -> Eb (row-major = E_a' column-major)
+      // (E_a E)^T = E^T E_a^T (row-major = E_a' column-major) into the slot
+      // of L, which the fold no longer reads
       zero(acc);
       mma<N, P_::TM, P_::TN, LD2, 1, LD, 1>(acc, Et + r0 * LD2, Ea + c0);
-      put<P_::TM, P_::TN, LD, 1>(Eb + r0 * LD + c0, acc);
+      put<P_::TM, P_::TN, LD, 1>(P + r0 * LD + c0, acc);
     }
   }
-  {
+  {  // E_a moves to L's slot; the old E_a slot becomes free (the caller's P)
     S* t = Ea;
-    Ea = Eb;
-    Eb = t;
+    Ea = P;
+    P = t;
   }
   gsync();
 }
@@ -497,7 +506,6 @@ __global__ void __launch_bounds__(kGW * kGroupsFinish)
   S* P = fr + FF::P0;
   S* Pn = fr + FF::P1;
   S* Ea = fr + FF::Ea0;
-  S* Eb = fr + FF::Ea1;
   // incoming filtered state: the prior (chunk 0) or the prefix of chunk c-1
   {
     const S* xs = c == 0 ? m.m0 : pre + (c - 1) * FO.size + FO.b;
@@ -513,7 +521,7 @@ __global__ void __launch_bounds__(kGW * kGroupsFinish)
     }
     t_predict<S, N, M>(fr, mf, P, Pn);
     if constexpr (SMOOTH) {
-      if (k > k0) t_smooth_elem<S, N, M>(fr, P, Ea, Eb, egl + (k - 1) * SO.size, k - 1 == k0, e);
+      if (k > k0) t_smooth_elem<S, N, M>(fr, P, Ea, egl + (k - 1) * SO.size, k - 1 == k0, e);
     }
     {  // x = xp, P = PP
       S* t = P;
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(kGW * kGroupsFinish)
         gsync();
       }
       t_predict<S, N, M>(fr, mf, P, Pn);
-      t_smooth_elem<S, N, M>(fr, P, Ea, Eb, egl + kl * SO.size, first, e);
+      t_smooth_elem<S, N, M>(fr, P, Ea, egl + kl * SO.size, first, e);
     }
     S* o = sagg + c * SO.size;
     gstore_mat<N, LD, true, false>(o + SO.E, Ea);  // E_a row-major from column-major
@@ -942,10 +950,14 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
   const int smem_f = cta_smem<S, N, M, FFrame<S, N, M>::size, kGroupsFinish>(inv);
   const int smem_s = (int)sizeof(S) * kGroupsSmooth * SFrame<S, N>::size;
   long long Lc = a.chunk;
-  if (Lc < 1) {  // auto: `waves` (default 4) waves of co-resident finish groups
+  // auto: `waves` waves of co-resident finish groups, default ONE -- a longer
+  // chunk amortises the per-chunk reduce and the scan, and the batch path's
+  // concurrent series fill the machine anyway (tools/config5.py --waves, f64
+  // 19.10 / 19.64 / 20.78 ms per series at 1 / 2 / 4 waves, batch 64)
+  if (Lc < 1) {
     const int per_sm = kernel_setup(k_t_finish<S, N, M, true>, kGW * kGroupsFinish, smem_f);
     const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
-                               kGroupsFinish * (a.waves > 0 ? a.waves : 4);
+                               kGroupsFinish * (a.waves > 0 ? a.waves : 1);
     Lc = (T + resident - 1) / resident;
     if (Lc < 1) Lc = 1;
   }

@@ -51,6 +51,7 @@ def main() -> None:
     ap.add_argument("--how", default="batch,loop")
     ap.add_argument("--tile", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--waves", type=int, default=0, help="auto chunk: waves of chunks (0: default)")
     args = ap.parse_args()
     from oracle.oracle import Oracle  # the reference's generator (inputs only)
     T, nx, ny = 1 << args.log2t, args.nx, args.ny
@@ -58,6 +59,8 @@ def main() -> None:
     stream = torch.cuda.Stream(device=dev)
     be = psk.CudaBackend(0, mode="fast", stream=stream)
     be.set_option("tile", args.tile)
+    if args.waves:
+        be.set_option("waves", args.waves)
     orc = Oracle("port")
     with ThreadPoolExecutor(16) as ex:
         seqs = list(ex.map(lambda b: model(orc, args.seed, b, nx, ny, T), range(args.batch)))
@@ -91,7 +94,7 @@ def main() -> None:
             ms = e0.elapsed_time(e1)
             print(json.dumps({"config": f"nx={nx} ny={ny} T=2^{args.log2t} batch={args.batch} "
                                         "time-invariant gen_model models, PRTS",
-                              "tile": args.tile,
+                              "tile": args.tile, "waves": args.waves,
                               "dtype": dts, "how": how, "ms_total": round(ms, 2),
                               "ms_per_sequence": round(ms / args.batch, 3),
                               "steps_per_s": args.batch * T / (ms * 1e-3)}), flush=True)
