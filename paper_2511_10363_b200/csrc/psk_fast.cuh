@@ -773,7 +773,7 @@ __device__ __forceinline__ SElem<S, NX> smoother_elem_pred(const Vec<S, NX>& x,
 // first step of a chunk the element computed from the incoming state belongs
 // to the previous chunk and is replaced by the identity.
 template <typename S, int NX, int NY, bool SMOOTH>
-__global__ void __launch_bounds__(kStageNT, 2)
+__global__ void __launch_bounds__(kStageNT, FilterTma<S, NX, NY>::finish_ctas)
     k_filter_finish(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
                     long long nchunks, long long nfull, const S* pre, long long pre_cap,
                     ChunkOrder pord, const S* carry, S* mean, S* cov, S* sagg,

@@ -191,9 +191,10 @@ long long auto_chunk(long long T, int waves, int mult = 1) {
   const int per_sm = kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT,
                                   FilterTma<S, NX, NY>::smem_n(FilterTma<S, NX, NY>::finish_stages));
   const long long wave = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) * kStageNT;
-  // default: 4 waves in FP64, 3 in FP32 (tools/waves_sweep.py, profiles/r01_v13:
-  // FP32 2.67 ms at 3 waves against 2.73 at 4; FP64 flat within 1 % over 4..8)
-  const int w = waves > 0 ? waves : (sizeof(S) == 4 ? 3 : 4);
+  // default: 6 waves (same-box chunk sweep at 2^24, profiles/r02_v4: FP32
+  // kernels 2.444 ms at 6 waves, 2.463 at 8, 2.557 at 3; FP64 4.47 at 6 and 8,
+  // 4.51-4.53 at 4).  Whole waves matter: 4.5 waves cost FP32 +12 %.
+  const int w = waves > 0 ? waves : 6;
   const long long L = (T + wave * w - 1) / (wave * w);
   // ... but at least 64 steps per chunk unless that leaves less than one
   // wave of chunks: short chunks make the per-chunk costs (incoming state,

@@ -164,7 +164,12 @@ struct FilterTma {
   // (28 KB each at nx = 4) still fit its 2 CTAs per SM (register-bound).
   // The reduce keeps two (3 CTAs/SM in FP32: measured faster than 2 x 3
   // stages; 4 stages fit only 1 CTA/SM, 2x slower).  FP64: two 53 KB stages.
-  static constexpr int finish_stages = sizeof(S) == 4 ? 3 : 2;
+  // FP32 takes a fourth stage where two CTAs still fit (nx = 4, ny <= 2)
+  // (2 stages at 3 CTAs/SM -- 168 registers, no spills -- measured 1.18 vs
+  // 1.115 ms, same box)
+  static constexpr int finish_stages =
+      sizeof(S) == 8 ? 2 : (2 * smem_n(4) <= 220 * 1024 ? 4 : 3);
+  static constexpr int finish_ctas = 2;
 };
 
 // this thread's row of a staged field <- a row-major R x C matrix (the
@@ -219,7 +224,9 @@ struct SmoothTma {
   // element stages of the per-warp pipeline: four (3 boxes in flight per
   // warp; FP64 2 CTAs/SM, FP32 4) -- measured against 2 and 3 stages:
   // FP64 1.165 / 1.133 / 1.116 ms, FP32 0.671 (2) / 0.629 ms (4) at 2^24
-  static constexpr int egl_nstage = 4;
+  // FP32 boxes are half as large: seven stages (3 CTAs/SM at nx = 4) keep
+  // about as many bytes in flight per SM as FP64's four
+  static constexpr int egl_nstage = sizeof(S) == 4 ? 7 : 4;
   // one warp: egl_nstage egl stages, 2 mean stages, 2 cov stages, mbarriers
   static constexpr int warp =
       egl_nstage * egl_stage + 2 * (mean_stage + cov_stage) + 1024;
