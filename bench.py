@@ -134,6 +134,52 @@ class ClockSampler:
                 "samples": len(self.sm), "source": "nvml"}
 
 
+class StreamGate:
+    """Holds a stream at a device-memory flag (cuStreamWaitValue32) while the
+    host queues the timed steps behind it, then releases it from a second
+    stream (cuStreamWriteValue32), so the K steps run back to back on the
+    device whatever the host thread does meanwhile.  Host-side stalls during
+    the enqueue (NVML clock polling contends with the driver; GIL hand-offs)
+    otherwise left the device idle now and then: 5.5 and 15.3 ms/step
+    against 4.43 on the same box.  A watchdog releases the gate after 30 s
+    in case the enqueue itself ever blocked.  Without cuda-python the timed
+    loop runs ungated (gate = False in the JSON line)."""
+
+    def __init__(self, stream, dev):
+        import torch
+        self.ok = False
+        try:
+            from cuda.bindings import driver as cu
+            self.cu = cu
+            self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.rel = torch.cuda.Stream(device=dev)
+            self.s = cu.CUstream(stream.cuda_stream)
+            self.addr = cu.CUdeviceptr(self.flag.data_ptr())
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            pass
+        self._released = threading.Event()
+
+    def close(self) -> None:
+        (err,) = self.cu.cuStreamWaitValue32(self.s, self.addr, 1, 0)
+        if err != self.cu.CUresult.CUDA_SUCCESS:
+            raise RuntimeError(f"cuStreamWaitValue32: {err}")
+        self._released.clear()
+        self._dog = threading.Timer(30.0, self.open)
+        self._dog.daemon = True
+        self._dog.start()
+
+    def open(self) -> None:
+        if self._released.is_set():
+            return
+        self._released.set()
+        self.cu.cuStreamWriteValue32(self.cu.CUstream(self.rel.cuda_stream), self.addr, 1, 0)
+
+    def reset(self) -> None:
+        self._dog.cancel()
+        self.flag.zero_()
+
+
 # algorithmic HBM bytes per time step for each fast-path kernel of PRTS
 # (DESIGN.md section 4): model inputs 52 scalars (nx=4, ny=2), per-step
 # smoothing elements (E, g, upper L) 30 scalars, smoothed stats 20 scalars
@@ -276,8 +322,8 @@ def spawn(args) -> int:
 
 class OracleRun(threading.Thread):
     """The CPU oracle's sequential kf_run + rts_run over the whole series (f64,
-    time-invariant blocks read with stride 0), started early on rank 0 so it
-    runs while the GPU is timed (the timed region is device time)."""
+    time-invariant blocks read with stride 0), on rank 0 after the timed
+    region."""
 
     def __init__(self, T: int, ys_np: np.ndarray):
         super().__init__(daemon=True)
@@ -379,8 +425,7 @@ def run_psk(args) -> None:
     ys_np = simulate_cv(T, seed=0)
     orc = None
     if not args.no_parity and rank == 0:
-        orc = OracleRun(T, ys_np)
-        orc.start()
+        orc = OracleRun(T, ys_np)  # started after the timed region (see below)
     lo, hi = dist_psk.shard_range(T, rank, world)
     hi_in = min(hi + 1, T)  # one extra transition for the smoother boundary
 
@@ -423,8 +468,13 @@ def run_psk(args) -> None:
     ev1 = torch.cuda.Event(enable_timing=True)
     be.set_profile(True)
     out = None
+    # (gloo -- the CPU test rig -- blocks the host on CUDA tensors: no gate)
+    gate = StreamGate(stream, dev) if pg is None or backend == "nccl" else None
+    gated = gate is not None and gate.ok
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if gated:
+            gate.close()  # the timed steps queue up behind the gate
         ev0.record(stream)
         h0 = time.perf_counter()
         for _ in range(args.steps):
@@ -432,7 +482,11 @@ def run_psk(args) -> None:
             launches += be.last_launch_count()
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue cost per step
         ev1.record(stream)
+        if gated:
+            gate.open()
         torch.cuda.synchronize()
+        if gated:
+            gate.reset()
     be.sync()  # raises on any device error of the timed steps
     be.set_profile(False)
     be.set_option("async", 0)
@@ -448,7 +502,12 @@ def run_psk(args) -> None:
     # ---- parity of the timed output against the CPU oracle (all T steps)
     parity = None
     if not args.no_parity:
+        # The oracle thread is NOT run during the timed region: its Python
+        # parts hold the GIL for long stretches, and every ctypes call of the
+        # enqueue loop must re-take it -- one run enqueued at 11 ms per step
+        # (15.3 ms/step on the device clock instead of 4.43).
         if orc is not None:
+            orc.start()
             orc.join()
         with torch.cuda.stream(stream):
             parity = parity_check(orc, out, lo, hi, T, dev, pg, rank, f64)
@@ -507,6 +566,9 @@ def run_psk(args) -> None:
             "roofline": roof, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels,
             "host_enqueue_ms_per_step": round(host_ms, 3),
+            "timing": ("the K steps queued behind a stream gate (cuStreamWaitValue32) and "
+                       "released together: CUDA events time device work only" if gated else
+                       "steps enqueued while the device runs (no gate)"),
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
