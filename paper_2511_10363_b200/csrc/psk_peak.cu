@@ -54,7 +54,66 @@ int run(int device, double* tflops, double* ms_out) {
   return 0;
 }
 
+// FP64 tensor-core MMA (mma.sync m8n8k4 f64, DMMA): 8 independent 8x8
+// accumulators per warp, operands in registers -- the ceiling a register-
+// fragment formulation of the nx = 16 products could reach
+__global__ void __launch_bounds__(256) k_dmma(double* out, int iters, double a0, double b0) {
+  double a = a0 + threadIdx.x * 1e-9, b = b0;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+            : "+d"(c[i][0]), "+d"(c[i][1])
+            : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == -12345.0) out[0] = s;
+}
+
+int run_dmma(int device, double* tflops, double* ms_out) {
+  cudaSetDevice(device);
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, device);
+  double* out;
+  cudaMalloc(&out, sizeof(double));
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 2048;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_dmma<<<blocks, threads>>>(out, 16, 1e-3, 1e-3);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_dmma<<<blocks, threads>>>(out, iters, 1e-3, 1e-3);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return 5;
+  // one m8n8k4 = 8 * 8 * 4 FMA = 512 flops per warp
+  const double flops = 512.0 * 32 * (double)iters * blocks * (threads / 32);
+  *tflops = flops / (best * 1e-3) / 1e12;
+  *ms_out = best;
+  return 0;
+}
+
 }  // namespace
+
+extern "C" int psk_peak_dmma(int device, double* tflops, double* ms) {
+  return run_dmma(device, tflops, ms);
+}
 
 extern "C" int psk_peak_fma(int device, int f64, double* tflops, double* ms) {
   return f64 ? run<double>(device, tflops, ms) : run<float>(device, tflops, ms);
