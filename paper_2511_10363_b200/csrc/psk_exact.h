@@ -34,6 +34,19 @@ int kernel_setup(Kernel kernel, int block, int smem) {
   cache[key] = per_sm;
   return per_sm;
 }
+// Chunk length floor of a Sequential chunk scan (psk_alg 0: one chain of
+// combines over the chunk elements, scan.hpp:198-210): the chain costs one
+// combine latency per chunk and each per-step walk one step latency per step
+// of a chunk, so about sqrt(T) chunks of sqrt(T) steps balance the two
+// (T = 2^14: 59 ms with 16384 one-step chunks, profiles/r02_v3/csv).
+inline long long seq_chunk_floor(long long T) {
+  long long s = 1;
+  while (s * s < T) s <<= 1;  // power-of-two bracket, then refine
+  long long lo = s >> 1;
+  while (lo * lo < T) ++lo;
+  return lo < 1 ? 1 : lo;
+}
+
 inline int device_sms() {
   static std::mutex mu;
   static std::map<int, int> cache;

@@ -237,6 +237,10 @@ static int fast_prepare_t(const ModelView<S>& m, const FastArgs& a, FastScratch<
                           void* (*alloc)(size_t, void*), void* actx) {
   const long long T = m.t;
   sc.chunk = a.chunk >= 1 ? a.chunk : auto_chunk<S, NX, NY>(T, a.waves, group_mult<S, NX, NY>(m));
+  if (a.chunk < 1 && a.alg == 0 && sc.chunk < seq_chunk_floor(T)) {
+    const long long mult = group_mult<S, NX, NY>(m);
+    sc.chunk = (seq_chunk_floor(T) + mult - 1) / mult * mult;
+  }
   sc.nchunks = T > 0 ? (T + sc.chunk - 1) / sc.chunk : 0;
   const bool dlb = a.alg == 6;
   sc.npad = (dlb || a.alg == 0) ? sc.nchunks : (long long)next_pow2(sc.nchunks);
@@ -451,8 +455,13 @@ static int fast_ptfs2_t(ExactLaunch& LA, const ModelView<S>& mA, int devA, Exact
                         void* (*allocB)(size_t, void*), void* ctxB) {
   if (mA.t == 0) return 0;
   a.method = 2;
-  if (a.chunk < 1)  // same L on both sides
+  if (a.chunk < 1) {  // same L on both sides
     a.chunk = auto_chunk<S, NX, NY>(mA.t, a.waves, group_mult<S, NX, NY>(mA));
+    if (a.alg == 0 && a.chunk < seq_chunk_floor(mA.t)) {
+      const long long mult = group_mult<S, NX, NY>(mA);
+      a.chunk = (seq_chunk_floor(mA.t) + mult - 1) / mult * mult;
+    }
+  }
   FastScratch<S> sa, sb;
   cudaSetDevice(devB);
   int st = fast_prepare_t<S, NX, NY>(mB, a, sb, allocB, ctxB);

@@ -960,6 +960,7 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
                                kGroupsFinish * (a.waves > 0 ? a.waves : 1);
     Lc = (T + resident - 1) / resident;
     if (Lc < 1) Lc = 1;
+    if (a.alg == 0 && Lc < seq_chunk_floor(T)) Lc = seq_chunk_floor(T);
   }
   const long long nch = (T + Lc - 1) / Lc;
   const int alg = a.alg == 6 ? 3 : a.alg;

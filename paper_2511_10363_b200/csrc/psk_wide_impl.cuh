@@ -635,7 +635,8 @@ int wide_run(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean, 
   if (T == 0) return 0;
   const int nx = m.nx;
   const int nm = step_slots(m);
-  const long long Lc = a.chunk >= 1 ? a.chunk : wide_auto_chunk<S>(T, a.waves, nm);
+  long long Lc = a.chunk >= 1 ? a.chunk : wide_auto_chunk<S>(T, a.waves, nm);
+  if (a.chunk < 1 && a.alg == 0 && Lc < seq_chunk_floor(T)) Lc = seq_chunk_floor(T);
   const long long nch = (T + Lc - 1) / Lc;
   const int alg = a.alg == 6 ? 3 : a.alg;
   const long long npad = alg == 0 ? nch : (long long)next_pow2(nch);

@@ -479,3 +479,24 @@ def test_contexts_from_concurrent_host_threads(psk, gpu, port):
     for t in th:
         t.join()
     assert not errs, errs
+
+
+def test_sequential_chunk_floor(psk, gpu, port):
+    """Sequential ScanAlg with the automatic chunk length: L is floored at
+    sqrt(T) (the chunk scan is one chain of combines, psk_exact.h
+    seq_chunk_floor) -- PKF / PRTS / PTFS on the nx = 4 fast path at
+    T = 2^17 (L = 363) and PRTS on the nx = 16 tiled path, vs the oracle."""
+    from paper_2511_10363_b200.synthetic import cv_model
+    from test_gpu_headline import _config5_series
+    m, ys = cv_model((1 << 17) + 5, seed=9)
+    kf, rts = port.kf_run(m, ys), port.rts_run(m, ys)
+    be = psk.CudaBackend(gpu)
+    spec = psk.ScanSpec(psk.ScanAlg.Sequential)
+    got = psk.pkf_run(m, ys, spec, be)
+    assert max_rel_err(got.mean, got.cov, *kf) < TOL64
+    for run in (psk.prts_run, psk.ptfs_run):
+        got = run(m, ys, spec, be)
+        assert max_rel_err(got.mean, got.cov, *rts) < TOL64, run.__name__
+    m16, ys16 = _config5_series(port, psk, 3, 1 << 13)
+    got = psk.prts_run(m16, ys16, spec, be)
+    assert max_rel_err(got.mean, got.cov, *port.rts_run(m16, ys16)) < TOL64
