@@ -132,12 +132,10 @@ __global__ void __launch_bounds__(kDlbThreads)
   const long long tile = s_tile;
   dlb_stamp(trace, tile, 0);
   // logical (x) on (buffer, index) pairs: reversed scans flip the operands
+  // (selected, not branched: one inlined combine per call site)
   auto lcomb = [&](const ElemBuf<S>& d, long long di, const ElemBuf<S>& l, long long li,
                    const ElemBuf<S>& r, long long ri) {
-    if (!rev)
-      ops.combine(d, di, l, li, r, ri);
-    else
-      ops.combine(d, di, r, ri, l, li);
+    ops.combine(d, di, rev ? r : l, rev ? ri : li, rev ? l : r, rev ? li : ri);
   };
   // slot of scan element g: the ChunkOrder of the buffer (perm: the tile
   // transpose, already in scan order) or the reference's Reversed map
