@@ -57,6 +57,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _spawn(fn, world, *rest):
+    """mp.spawn with a fresh rendezvous port; retried when another process
+    took the port between _free_port() and the bind (EADDRINUSE)."""
+    import torch.multiprocessing as mp
+    for attempt in range(3):
+        try:
+            mp.spawn(fn, args=(world, _free_port(), *rest), nprocs=world, join=True)
+            return
+        except Exception as e:  # noqa: BLE001
+            msg = str(e)
+            if attempt == 2 or ("Address already in use" not in msg and "EADDRINUSE" not in msg):
+                raise
+
+
 @pytest.fixture(scope="module")
 def rts_ref(port):
     from paper_2511_10363_b200.synthetic import cv_model
@@ -68,7 +82,7 @@ def rts_ref(port):
 def test_prts_run_sharded_processes(gpu, tmp_path, rts_ref, world, alg):
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), alg), nprocs=world, join=True)
+    _spawn(_worker, world, str(tmp_path), alg)
     rm, rc = rts_ref
     covered = 0
     for r in range(world):
@@ -116,7 +130,7 @@ def test_config5_batch_sharded_processes(gpu, tmp_path, port):
     from test_gpu_headline import _config5_series
 
     world = 2
-    mp.spawn(_batch_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_batch_worker, world, str(tmp_path))
     seen = []
     for r in range(world):
         d = np.load(tmp_path / f"b{r}.npz")
@@ -165,7 +179,7 @@ def test_ptfs_halves_processes(gpu, tmp_path, port, world):
     import torch.multiprocessing as mp
 
     from paper_2511_10363_b200.synthetic import cv_model
-    mp.spawn(_ptfs_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    _spawn(_ptfs_worker, world, str(tmp_path))
     m, ys = cv_model(T, seed=23)
     rm, rc = port.rts_run(m, ys)
     covered = 0

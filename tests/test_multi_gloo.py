@@ -174,12 +174,26 @@ def _free_port():
     return p
 
 
+def _spawn(fn, world, *rest):
+    """mp.spawn with a fresh rendezvous port; retried when another process
+    took the port between _free_port() and the bind (EADDRINUSE)."""
+    import torch.multiprocessing as mp
+    for attempt in range(3):
+        try:
+            mp.spawn(fn, args=(world, _free_port(), *rest), nprocs=world, join=True)
+            return
+        except Exception as e:  # noqa: BLE001
+            msg = str(e)
+            if attempt == 2 or ("Address already in use" not in msg and "EADDRINUSE" not in msg):
+                raise
+
+
 @pytest.mark.parametrize("world,t", [(2, 101), (3, 64)])
 def test_sharded_prts_matches_sequential(tmp_path, port, world, t):
     import torch.multiprocessing as mp
 
     from conftest import gen, max_rel_err
-    mp.spawn(_worker, args=(world, _free_port(), t, str(tmp_path)), nprocs=world, join=True)
+    _spawn(_worker, world, t, str(tmp_path))
     m, ys = gen(port, 12, 4, 2, t)
     rm, rc = port.rts_run(m, ys)
     covered = 0
@@ -263,8 +277,7 @@ def test_sharded_ptfs_halves_matches_rts(tmp_path, port, world, t):
     import torch.multiprocessing as mp
 
     from conftest import gen, max_rel_err
-    mp.spawn(_ptfs_worker, args=(world, _free_port(), t, str(tmp_path)), nprocs=world,
-             join=True)
+    _spawn(_ptfs_worker, world, t, str(tmp_path))
     m, ys = gen(port, 14, 4, 2, t)
     rm, rc = port.rts_run(m, ys)
     covered = 0
