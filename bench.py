@@ -290,6 +290,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="enqueue the timed steps while the device runs (no stream gate)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -468,8 +470,13 @@ def run_psk(args) -> None:
     ev1 = torch.cuda.Event(enable_timing=True)
     be.set_profile(True)
     out = None
-    # (gloo -- the CPU test rig -- blocks the host on CUDA tensors: no gate)
-    gate = StreamGate(stream, dev) if pg is None or backend == "nccl" else None
+    # (gloo -- the CPU test rig -- blocks the host on CUDA tensors: no gate;
+    # under a profiler (ncu serialises every launch: the first gated launch
+    # would never return) or with --no-gate the steps run ungated)
+    profiled = any(k in os.environ for k in ("CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN",
+                                             "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+    gate = (StreamGate(stream, dev) if (pg is None or backend == "nccl") and not profiled
+            and not args.no_gate else None)
     gated = gate is not None and gate.ok
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()

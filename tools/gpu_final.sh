@@ -7,7 +7,7 @@
 set -u
 O=gpurun_out/${1:-final}
 mkdir -p $O
-Q="--steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-parity"
+Q="--steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-parity --no-gate"
 timeout 900 python bench.py > $O/bench_f64.log 2>&1; tail -c 400 $O/bench_f64.log; echo
 timeout 900 python bench.py --dtype f32 --no-cpu-baseline > $O/bench_f32.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

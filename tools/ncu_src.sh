@@ -11,7 +11,7 @@ K=${3:-k_filter_reduce|k_filter_finish|k_smoother_finish}
 mkdir -p $O
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$K" -s ${4:-3} -c ${5:-3} -f \
   -o /tmp/src_prof python bench.py --dtype $D --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
-  --no-parity > $O/ncu_$D.log 2>&1
+  --no-parity --no-gate > $O/ncu_$D.log 2>&1
 ncu -i /tmp/src_prof.ncu-rep --page raw --csv > $O/${D}_raw.csv 2>&1
 for k in $(echo $K | tr '|' ' '); do
   ncu -i /tmp/src_prof.ncu-rep -k "regex:$k" --page source --csv --print-source sass \
