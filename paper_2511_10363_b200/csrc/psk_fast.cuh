@@ -61,20 +61,28 @@ struct EglLayout {
   static constexpr int E = 0, g = NX * NX, L = NX * NX + NX,
                        size = NX * NX + NX + NX * (NX + 1) / 2;
 };
+// (global = false: plain stores, e.g. into shared memory)
 template <typename S, int NX>
-__device__ __forceinline__ void egl_store(S* p, long long cap, const SElem<S, NX>& e) {
+__device__ __forceinline__ void egl_store(S* p, long long cap, const SElem<S, NX>& e,
+                                          bool global = true) {
   using Lo = EglLayout<NX>;
+  auto put = [&](int comp, S v) {
+    if (global)
+      __stcs(p + comp * cap, v);
+    else
+      p[comp * cap] = v;
+  };
 #pragma unroll
   for (int i = 0; i < NX; ++i)
 #pragma unroll
-    for (int j = 0; j < NX; ++j) __stcs(p + (Lo::E + i * NX + j) * cap, e.E.a[i][j]);
+    for (int j = 0; j < NX; ++j) put(Lo::E + i * NX + j, e.E.a[i][j]);
 #pragma unroll
-  for (int i = 0; i < NX; ++i) __stcs(p + (Lo::g + i) * cap, e.g.a[i][0]);
+  for (int i = 0; i < NX; ++i) put(Lo::g + i, e.g.a[i][0]);
   int q = Lo::L;
 #pragma unroll
   for (int i = 0; i < NX; ++i)
 #pragma unroll
-    for (int j = i; j < NX; ++j) __stcs(p + (q++) * cap, e.L.a[i][j]);
+    for (int j = i; j < NX; ++j) put(q++, e.L.a[i][j]);
 }
 template <typename S, int NX>
 __device__ __forceinline__ SElem<S, NX> egl_load(const S* p, long long cap) {
@@ -504,10 +512,17 @@ struct FilterStage {
 // walk is CTA-uniform (every thread of the CTA must call it: block barriers),
 // of length min(L, T - first step of the CTA).  `nfull` = number of complete
 // chunks (the extent of the tensor maps).
-template <typename S, int NX, int NY, int NS = 2, class Body>
+struct NoPost {
+  __device__ void operator()(unsigned char*, long long) const {}
+};
+// `post(stage, j)` runs on thread 0 of a TMA CTA once the CTA has finished
+// walk position j (after its block barrier), before the stage is refilled:
+// the body may leave results in the consumed stage for a TMA store.
+template <typename S, int NX, int NY, int NS = 2, class Body, class Post = NoPost>
 __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const StageMaps& maps,
                                             const ModelView<S>& m, long long L, long long nfull,
-                                            long long k0, long long k1, Body&& body) {
+                                            long long k0, long long k1, Body&& body,
+                                            Post post = Post{}) {
   using In = FilterTma<S, NX, NY>;
   using St = FilterStage<S, NX, NY>;
   unsigned char* sm = reinterpret_cast<unsigned char*>(
@@ -550,7 +565,11 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
   unsigned phase = 0;  // its mbarrier phase
   for (long long j = 0; j < jn; ++j) {
     // refill the stage consumed at j - 1 (all threads passed the barrier)
-    if (tma && t == 0 && j + NS - 1 < jn) issue(s == 0 ? NS - 1 : s - 1, j + NS - 1);
+    if (tma && t == 0) {
+      const int sp = s == 0 ? NS - 1 : s - 1;
+      if (j > 0) post(sm + sp * In::stage, j - 1);
+      if (j + NS - 1 < jn) issue(sp, j + NS - 1);
+    }
     if (tma) mbar_wait(&bars[s], phase);
     if (k0 + j < k1) body(k0 + j, St{sm + s * In::stage, t, direct, &m, k0 + j, unstaged, g2, g4, (int)j});
     __syncthreads();  // stage s is refilled by the next iteration's issue
@@ -559,6 +578,7 @@ __device__ __forceinline__ void staged_walk(unsigned char* smem_raw, const Stage
       phase ^= 1u;
     }
   }
+  if (tma && t == 0 && jn > 0) post(sm + (s == 0 ? NS - 1 : s - 1) * In::stage, jn - 1);
 }
 
 // The same multi-buffered TMA walk, backwards: positions j = jn-1 .. 0 of
@@ -777,7 +797,8 @@ __global__ void __launch_bounds__(kStageNT, FilterTma<S, NX, NY>::finish_ctas)
     k_filter_finish(ModelView<S> m, const __grid_constant__ StageMaps maps, long long L,
                     long long nchunks, long long nfull, const S* pre, long long pre_cap,
                     ChunkOrder pord, const S* carry, S* mean, S* cov, S* sagg,
-                    long long scap, ChunkOrder sord, S* egl, long long ecap, unsigned* err) {
+                    long long scap, ChunkOrder sord, S* egl, long long ecap, unsigned* err,
+                    const __grid_constant__ EglStore em) {
   extern __shared__ __align__(1024) unsigned char fsm[];
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = c < nchunks;  // idle threads stay for the block barriers
@@ -790,6 +811,18 @@ __global__ void __launch_bounds__(kStageNT, FilterTma<S, NX, NY>::finish_ctas)
   Mat<S, NX, NX> P = zeros<S, NX, NX>();
   if (live) filter_incoming<S, NX>(m, c, pre, pre_cap, pord, carry, x, P, e);
   SElem<S, NX> sa = se_identity<S, NX>();
+  // PRTS: in CTAs whose 128 chunks are all complete, step k's element e_{k-1}
+  // goes to the consumed input stage (its F / u / Q boxes, read at the start
+  // of the step) and leaves by one TMA store per walk position, instead of
+  // 30 scattered 8-byte stores per thread
+  const bool egl_tma = SMOOTH && em.use && ((long long)blockIdx.x + 1) * kStageNT <= nfull;
+  auto post = [&](unsigned char* st, long long j) {
+    if (egl_tma && j >= 1) {
+      tma_store_2d(&em.map, (int)(blockIdx.x * kStageNT), (int)((j - 1) * ES), st);
+      bulk_commit();
+      bulk_wait_read<0>();  // the stage is refilled next
+    }
+  };
   staged_walk<S, NX, NY, FilterTma<S, NX, NY>::finish_stages>(
       fsm, maps, m, L, nfull, k0, k1, [&](long long k, const St& in) {
     const Mat<S, NX, NX> F = in.F();
@@ -814,7 +847,18 @@ __global__ void __launch_bounds__(kStageNT, FilterTma<S, NX, NY>::finish_ctas)
         }
       }
       sa = smoother_combine(sa, eu);
-      if (keep) egl_store(egl + (k - 1 - k0) * ES * ecap + c, ecap, ek);
+      if (egl_tma) {
+        if (keep) {  // CTA-uniform (k - k0 is the walk position)
+          // every thread's F / u / Q rows are read before any thread writes
+          // over them (the element rows span all chunks' input rows)
+          __syncthreads();
+          S* es = reinterpret_cast<S*>(const_cast<unsigned char*>(in.st));
+          egl_store(es + threadIdx.x, (long long)kStageNT, ek, false);
+          fence_proxy_async();  // generic writes -> the async proxy (TMA store)
+        }
+      } else if (keep) {
+        egl_store(egl + (k - 1 - k0) * ES * ecap + c, ecap, ek);
+      }
     }
     x = xp;
     P = pp;
@@ -825,8 +869,9 @@ __global__ void __launch_bounds__(kStageNT, FilterTma<S, NX, NY>::finish_ctas)
       else
         state_store(egl + (k - k0) * StateLayout<NX>::size * ecap + c, ecap, x, P);
     }
-  });
+  }, post);
   if constexpr (SMOOTH) {
+    if (egl_tma && threadIdx.x == 0) bulk_wait<0>();
     if (live) {  // element of the chunk's last step
       SElem<S, NX> ek;
       if (k1 - 1 == m.last_step)

@@ -330,16 +330,21 @@ static int fast_phase_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a
       break;
     case 1:  // filter finish; for PRTS also folds the smoother chunk elements
       if (a.method == 1) {
+        EglStore em;
+        const int st = make_egl_store_map<S, NX, NY>(sc.egl, sc.ecap, Lc, em);
+        if (st) return st;
         kernel_setup(k_filter_finish<S, NX, NY, true>, kStageNT, finish_bytes);
         k_filter_finish<S, NX, NY, true><<<gs, kStageNT, finish_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, sc.cap, sc.ford, carry, mean, cov, sc.sagg,
-            sc.cap, sc.sord, sc.egl, sc.ecap, L.err);
+            sc.cap, sc.sord, sc.egl, sc.ecap, L.err, em);
         L.count("filter_finish_smoother_reduce");
       } else {
+        EglStore em;
+        em.use = 0;
         kernel_setup(k_filter_finish<S, NX, NY, false>, kStageNT, finish_bytes);
         k_filter_finish<S, NX, NY, false><<<gs, kStageNT, finish_bytes, L.stream>>>(
             m, maps, Lc, nch, nfull, sc.agg, sc.cap, sc.ford, carry, mean, cov, nullptr,
-            sc.cap, sc.sord, a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err);
+            sc.cap, sc.sord, a.method == 2 ? sc.egl : nullptr, sc.ecap, L.err, em);
         L.count("filter_finish");
       }
       sc.sagg_valid = a.method == 1;

@@ -78,6 +78,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int
       "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1,
+                                             const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          map),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -188,6 +196,15 @@ __device__ __forceinline__ void tma_put(unsigned char* stage, int t, const Mat<S
     *reinterpret_cast<float4*>(stage + F::off + tma_off<F>(t, c)) = v;
   }
 }
+
+// TMA store of the PRTS filter finish's per-step smoothing elements: the
+// chunk-interleaved egl buffer as a 2-D tensor [ecap, ES * L] written one
+// walk position of the CTA's 128 chunks at a time (box {kStageNT, ES}) from
+// the consumed input stage (kernel parameter; use = 0: plain stores).
+struct EglStore {
+  CUtensorMap map;
+  int use;
+};
 
 // Tensor maps of the seven model fields for one staged launch (kernel
 // parameter; `use[f]` = 0 for a broadcast field, read straight from global).

@@ -108,6 +108,37 @@ int make_stage_maps(const ModelView<S>& m, long long L, long long nfull, StageMa
   return 0;
 }
 
+// The filter finish's egl store map (EglStore): box {kStageNT chunks, ES
+// components} of the [ecap, ES * L] egl tensor, staged in the first ES *
+// kStageNT scalars of a consumed input stage (F, u, Q -- read at the start of
+// a step) -- only where that region ends before H's box.  FP32 only: the
+// extra block barrier per step (the element rows span every chunk's input
+// rows) costs FP64 more than the saved stores (same box, 2^24: FP64 finish
+// 1.983 -> 2.018 ms, FP32 1.016 -> 0.9996 ms; profiles/r02_v4/small_t.txt)
+template <typename S, int NX, int NY>
+int make_egl_store_map(S* egl, long long ecap, long long L, EglStore& em) {
+  using In = FilterTma<S, NX, NY>;
+  constexpr int ES = NX * NX + NX + NX * (NX + 1) / 2;
+  em.use = 0;
+  if (sizeof(S) != 4 || egl == nullptr || ES > 256 ||
+      ES * kStageNT * (int)sizeof(S) > In::off(3) ||
+      reinterpret_cast<uintptr_t>(egl) % 16 || (ecap * sizeof(S)) % 16)
+    return 0;
+  auto enc = tma_encoder();
+  if (!enc) return 9;
+  cuuint64_t dims[2] = {(cuuint64_t)ecap, (cuuint64_t)(ES * L)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ecap * sizeof(S))};
+  cuuint32_t box[2] = {(cuuint32_t)kStageNT, (cuuint32_t)ES};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(&em.map, sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+          2, egl, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 9;
+  em.use = 1;
+  return 0;
+}
+
 // Tensor maps of the smoother finish: the chunk-interleaved per-step
 // elements egl[(j * ES + comp) * ecap + c] as a 2-D tensor [ecap, ES * L]
 // (box {32, ES}) and the outputs mean[T][NX], cov[T][NX][NX] as 3-D tensors
