@@ -61,18 +61,19 @@ def _peaks() -> dict:
 
 def _traffic(kernel: str, log2t: int, dtype: str, chunk: int) -> tuple:
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture (profiles/traffic.json, written by tools/ncu_summary.py --json) when
+    capture (profiles/traffic.json, FP32: traffic_f32.json, written by
+    tools/ncu_summary.py --json) when
     it was taken on this workload; (None, None) otherwise."""
-    p = ROOT / "profiles" / "traffic.json"
-    try:
-        d = json.loads(p.read_text())
-        w = d["workload"]
-        if w["log2t"] == log2t and w["dtype"] == dtype and w["chunk"] == chunk:
-            k = d["kernels"].get(kernel)
-            if k is not None:
-                return float(k["dram_bytes"]), d["source"]
-    except (OSError, KeyError, ValueError):
-        pass
+    for name in ("traffic.json", "traffic_f32.json"):
+        try:
+            d = json.loads((ROOT / "profiles" / name).read_text())
+            w = d["workload"]
+            if w["log2t"] == log2t and w["dtype"] == dtype and w["chunk"] == chunk:
+                k = d["kernels"].get(kernel)
+                if k is not None:
+                    return float(k["dram_bytes"]), d["source"]
+        except (OSError, KeyError, ValueError):
+            pass
     return None, None
 
 

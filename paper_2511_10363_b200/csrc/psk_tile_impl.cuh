@@ -950,14 +950,17 @@ int tile_run_t(ExactLaunch& L, const ModelView<S>& m, const FastArgs& a, S* mean
   const int smem_f = cta_smem<S, N, M, FFrame<S, N, M>::size, kGroupsFinish>(inv);
   const int smem_s = (int)sizeof(S) * kGroupsSmooth * SFrame<S, N>::size;
   long long Lc = a.chunk;
-  // auto: `waves` waves of co-resident finish groups, default ONE -- a longer
-  // chunk amortises the per-chunk reduce and the scan, and the batch path's
-  // concurrent series fill the machine anyway (tools/config5.py --waves, f64
-  // 19.10 / 19.64 / 20.78 ms per series at 1 / 2 / 4 waves, batch 64)
+  // auto: `waves` waves of co-resident finish groups, default ONE for PKF /
+  // PRTS -- a longer chunk amortises the per-chunk reduce and the scan, and
+  // the batch path's concurrent series fill the machine anyway
+  // (tools/config5.py --waves, f64 19.10 / 19.64 / 20.78 ms per series at
+  // 1 / 2 / 4 waves, batch 64) -- and FOUR for PTFS, whose backward finish
+  // holds fewer groups per SM (f64 60.7 / 51.3 / 51.5 / 54.3 ms per series at
+  // 1 / 2 / 4 / 8 waves, f32 28.4 / 24.5 / 23.0 / 24.3; 3 waves: 56.7 f64)
   if (Lc < 1) {
     const int per_sm = kernel_setup(k_t_finish<S, N, M, true>, kGW * kGroupsFinish, smem_f);
     const long long resident = (long long)device_sms() * (per_sm > 0 ? per_sm : 1) *
-                               kGroupsFinish * (a.waves > 0 ? a.waves : 1);
+                               kGroupsFinish * (a.waves > 0 ? a.waves : (a.method == 2 ? 4 : 1));
     Lc = (T + resident - 1) / resident;
     if (Lc < 1) Lc = 1;
     if (a.alg == 0 && Lc < seq_chunk_floor(T)) Lc = seq_chunk_floor(T);

@@ -52,6 +52,8 @@ def main() -> None:
     ap.add_argument("--tile", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--waves", type=int, default=0, help="auto chunk: waves of chunks (0: default)")
+    ap.add_argument("--method", default="prts", choices=["prts", "pkf", "ptfs"],
+                    help="ptfs runs one call per sequence (no batch entry point)")
     args = ap.parse_args()
     from oracle.oracle import Oracle  # the reference's generator (inputs only)
     T, nx, ny = 1 << args.log2t, args.nx, args.ny
@@ -75,25 +77,29 @@ def main() -> None:
         outs = [psk.GaussianStats(torch.empty((T, nx), dtype=tdt, device=dev),
                                   torch.empty((T, nx, nx), dtype=tdt, device=dev))
                 for _ in range(args.batch)]
+        single = {"prts": psk.prts_run, "pkf": psk.pkf_run, "ptfs": psk.ptfs_run}[args.method]
+        batch = {"prts": psk.prts_run_batch, "pkf": psk.pkf_run_batch}.get(args.method)
         with torch.cuda.stream(stream):
-            psk.prts_run(ms_[0], ys_[0], spec, be, out=outs[0])  # warm-up
-            psk.prts_run_batch(ms_, ys_, spec, be, outs=outs)
+            single(ms_[0], ys_[0], spec, be, out=outs[0])  # warm-up
+            if batch is not None:
+                batch(ms_, ys_, spec, be, outs=outs)
         torch.cuda.synchronize()
         for how in args.how.split(","):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
                 e0.record(stream)
-                if how == "loop":  # one synchronous call per sequence
+                if how == "loop" or batch is None:  # one synchronous call per sequence
+                    how = "loop"
                     for m, ys, o in zip(ms_, ys_, outs):
-                        psk.prts_run(m, ys, spec, be, out=o)
-                else:  # one psk_prts_batch call (sub-streams)
-                    psk.prts_run_batch(ms_, ys_, spec, be, outs=outs)
+                        single(m, ys, spec, be, out=o)
+                else:  # one psk_prts_batch / psk_pkf_batch call (sub-streams)
+                    batch(ms_, ys_, spec, be, outs=outs)
                 e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
             print(json.dumps({"config": f"nx={nx} ny={ny} T=2^{args.log2t} batch={args.batch} "
-                                        "time-invariant gen_model models, PRTS",
+                                        f"time-invariant gen_model models, {args.method.upper()}",
                               "tile": args.tile, "waves": args.waves,
                               "dtype": dts, "how": how, "ms_total": round(ms, 2),
                               "ms_per_sequence": round(ms / args.batch, 3),

@@ -18,5 +18,11 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 python tools/ncu_summary.py $O/launches.csv /tmp/prts_prof.ncu-rep > $O/ncu_summary.txt 2>&1
 python tools/ncu_summary.py --json /tmp/prts_prof.ncu-rep "profiles/$1/ncu_summary.txt" 24 f64 0 \
   > $O/traffic.json 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k "regex:k_filter_reduce|k_filter_finish|k_smoother_finish" -s 3 -c 3 -f -o /tmp/prts_prof32 \
+  python bench.py $Q --dtype f32 > $O/ncu_full_f32.log 2>&1
+python tools/ncu_summary.py --full /tmp/prts_prof32.ncu-rep > $O/ncu_summary_f32.txt 2>&1
+python tools/ncu_summary.py --json /tmp/prts_prof32.ncu-rep "profiles/$1/ncu_summary_f32.txt" 24 f32 0 \
+  > $O/traffic_f32.json 2>&1
 timeout 900 python tools/config5.py --batch 64 --dtypes f64,f32 --how batch > $O/config5.jsonl 2>&1
 ls -la $O

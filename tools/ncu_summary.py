@@ -122,6 +122,9 @@ if __name__ == "__main__":
                                       {"log2t": int(sys.argv[4]), "dtype": sys.argv[5],
                                        "chunk": int(sys.argv[6])}), indent=1))
         sys.exit(0)
+    if sys.argv[1] == "--full":  # --full <prof.ncu-rep>: the --set full counters only
+        print(full(sys.argv[2]))
+        sys.exit(0)
     print(launches(sys.argv[1]))
     if len(sys.argv) > 2:
         print()
