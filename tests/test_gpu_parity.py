@@ -500,3 +500,20 @@ def test_sequential_chunk_floor(psk, gpu, port):
     m16, ys16 = _config5_series(port, psk, 3, 1 << 13)
     got = psk.prts_run(m16, ys16, spec, be)
     assert max_rel_err(got.mean, got.cov, *port.rts_run(m16, ys16)) < TOL64
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (2, 1), (3, 2), (4, 1), (4, 4)])
+def test_fast_f32_prts_dims(psk, gpu, port, nx, ny):
+    """FP32 PRTS through the fast path at every nx <= 4 with whole CTAs of
+    complete chunks (T = 2^15: the finish's per-step elements leave by TMA
+    box stores where they fit the consumed stage, psk_tma.hpp
+    make_egl_store_map), vs the f64 sequential oracle.  On random gen_model
+    data the reference's own FP32 error is 1e-5..1e-4 (see
+    test_fast_f32_random_model_vs_reference_f32), hence 10x the tracking
+    model's FP32 gate."""
+    m, ys = gen(port, 500 + nx * 10 + ny, nx, ny, 1 << 15)
+    rts = port.rts_run(m, ys)
+    m32, ys32 = _cast(m, ys, np.float32)
+    be = psk.CudaBackend(gpu)
+    got = psk.prts_run(m32, ys32, psk.ScanSpec(psk.ScanAlg.DecoupledLookback), be)
+    assert max_rel_err(got.mean, got.cov, *rts) < TOL32 * 10, (nx, ny)
